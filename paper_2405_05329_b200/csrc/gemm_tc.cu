@@ -1,0 +1,327 @@
+// gemm_tc.cu -- the projection GEMMs of the per-rank layer executor on 5th-gen tensor
+// cores (reference sites: qkv_project model.hpp:65-73, A.Wo / f.W1 / mid.W2 model.hpp:172-174,
+// all through matrix.hpp:76-91 matmul).
+//
+// D[M x N] = A[M x K] . B[N x K]^T, bf16 operands, f32 accumulation in TMEM.
+//  * persistent: one CTA per SM (grid = min(#tiles, #SMs)), static round-robin tile order,
+//    M-fastest rasterisation so the CTAs in flight share the same weight columns in L2;
+//  * warp roles (192 threads): warp 0 = TMA producer (one lane), warp 1 = tcgen05.mma
+//    issuer (one lane) + TMEM owner, warps 2..5 = epilogue (TMEM -> registers -> global);
+//  * 4-stage smem ring of 128 x 64 (A) and BN x 64 (B) bf16 tiles, 128-byte swizzle,
+//    full/empty mbarriers; MMA completion frees a stage via tcgen05.commit;
+//  * two TMEM accumulators (2 x BN columns) so the epilogue of tile t overlaps the MMAs
+//    of tile t+1;
+//  * fused epilogues: Q/K/V split store straight into the rank's KV-cache rows (replaces
+//    the reference's vcat, engine.hpp:277-278), f32 residual add, ReLU + bf16 cast.
+// Operand tails (M, N, K not multiples of the tile) are zero-filled by TMA; the epilogue
+// predicates rows and columns.
+#include <cstdio>
+#include <mutex>
+#include <stdexcept>
+
+#include "kernels.cuh"
+#include "ptx.cuh"
+
+namespace kvp {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int STAGES = 4;
+constexpr int THREADS = 192;
+
+template <int BN>
+struct Cfg {
+    static constexpr uint32_t A_BYTES = BM * BK * 2;
+    static constexpr uint32_t B_BYTES = BN * BK * 2;
+    static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr uint32_t TMEM_COLS = 2 * BN;
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+struct EpiArgs {
+    bf16* out0;
+    int64_t ld0, n0;
+    bf16* out1;
+    int64_t ld1, n1;
+    bf16* out2;
+    int64_t ld2;
+    float* outf;
+    int64_t ldf;
+    const float* resid;
+    int64_t ldr;
+};
+
+template <int KIND>
+__device__ __forceinline__ void store_chunk(const EpiArgs& ep, int64_t row, int64_t col0, int64_t N,
+                                            const uint32_t (&r)[32]) {
+    const bool full = col0 + 32 <= N;
+    if constexpr (KIND == EPI_RESID) {
+        float* o = ep.outf + row * ep.ldf + col0;
+        const float* rs = ep.resid + row * ep.ldr + col0;
+        if (full) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+                const float4 a = *reinterpret_cast<const float4*>(rs + j);
+                float4 v;
+                v.x = a.x + __uint_as_float(r[j + 0]);
+                v.y = a.y + __uint_as_float(r[j + 1]);
+                v.z = a.z + __uint_as_float(r[j + 2]);
+                v.w = a.w + __uint_as_float(r[j + 3]);
+                *reinterpret_cast<float4*>(o + j) = v;
+            }
+        } else {
+            for (int j = 0; j < 32 && col0 + j < N; ++j) o[j] = rs[j] + __uint_as_float(r[j]);
+        }
+    } else {
+        bf16* o;
+        if constexpr (KIND == EPI_QKV) {
+            if (col0 < ep.n0) {
+                o = ep.out0 + row * ep.ld0 + col0;
+            } else if (col0 < ep.n0 + ep.n1) {
+                o = ep.out1 + row * ep.ld1 + (col0 - ep.n0);
+            } else {
+                o = ep.out2 + row * ep.ld2 + (col0 - ep.n0 - ep.n1);
+            }
+        } else {
+            o = ep.out0 + row * ep.ld0 + col0;
+        }
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            v[j] = __uint_as_float(r[j]);
+            if constexpr (KIND == EPI_RELU) v[j] = v[j] < 0.f ? 0.f : v[j];
+        }
+        if (full) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+                uint4 pk;
+                pk.x = ptx::pack_bf16(v[j + 0], v[j + 1]);
+                pk.y = ptx::pack_bf16(v[j + 2], v[j + 3]);
+                pk.z = ptx::pack_bf16(v[j + 4], v[j + 5]);
+                pk.w = ptx::pack_bf16(v[j + 6], v[j + 7]);
+                *reinterpret_cast<uint4*>(o + j) = pk;
+            }
+        } else {
+            for (int j = 0; j < 32 && col0 + j < N; ++j) o[j] = __float2bfloat16_rn(v[j]);
+        }
+    }
+}
+
+template <int BN, int KIND>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                   int K, EpiArgs ep) {
+    using C = Cfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * C::A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
+    const int num_tiles = num_m * num_n;
+    const int num_kb = (K + BK - 1) / BK;
+
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&tmA);
+        ptx::tma_prefetch_desc(&tmB);
+        for (int s = 0; s < STAGES; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&tfull[b], 1);
+            ptx::mbar_init(&tempty[b], 4);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 1) ptx::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                const int m_blk = tile % num_m, n_blk = tile / num_m;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    ptx::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+                    ptx::tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+                    ptx::tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_bf16(BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int t = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+                const uint32_t buf = t & 1, aphase = (t >> 1) & 1;
+                ptx::mbar_wait(&tempty[buf], aphase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + buf * BN;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a0 = ptx::smem_u32(sA + stage * C::A_BYTES);
+                    const uint32_t b0 = ptx::smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        const uint64_t ad = ptx::smem_desc_sw128(a0 + k * 32, 16, 1024);
+                        const uint64_t bd = ptx::smem_desc_sw128(b0 + k * 32, 16, 1024);
+                        ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                    }
+                    ptx::mma_commit(&empty[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                ptx::mma_commit(&tfull[buf]);
+            }
+        }
+    } else {
+        // Epilogue warps 2..5: warp w may touch TMEM lanes [32*(w%4), 32*(w%4)+32).
+        const uint32_t quarter = warp & 3;
+        int t = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+            const int m_blk = tile % num_m, n_blk = tile / num_m;
+            const uint32_t buf = t & 1, aphase = (t >> 1) & 1;
+            ptx::mbar_wait(&tfull[buf], aphase);
+            ptx::tc_fence_after();
+            const int64_t row = static_cast<int64_t>(m_blk) * BM + quarter * 32 + lane;
+            const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + buf * BN;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                const int64_t col0 = static_cast<int64_t>(n_blk) * BN + c * 32;
+                if (col0 >= N) break;  // warp-uniform
+                uint32_t r[32];
+                ptx::tmem_ld32(taddr + c * 32, r);
+                ptx::tmem_ld_wait();
+                if (row < M) store_chunk<KIND>(ep, row, col0, N, r);
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[buf]);
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+    }
+}
+
+// ------------------------------------------------------------------ host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    return fn;
+}
+
+// 2D bf16 tensor [outer x inner] with row stride ld (elements), box [box_outer x 64],
+// 128-byte swizzle (the canonical K-major SW128 UMMA layout).
+bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+                    uint32_t box_inner, uint32_t box_outer) {
+    EncodeFn enc = get_encode();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {inner, outer};
+    const cuuint64_t strides[1] = {ld * 2};
+    const cuuint32_t box[2] = {box_inner, box_outer};
+    const cuuint32_t estr[2] = {1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int num_sms() {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+}
+
+template <int BN, int KIND>
+void launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const EpiArgs& ep,
+               cudaStream_t s) {
+    auto kern = gemm_tc_kernel<BN, KIND>;
+    static thread_local int configured_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured_dev != dev) {  // attribute is per device; cheap to re-set
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM);
+        configured_dev = dev;
+    }
+    const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+    const int grid = tiles < num_sms() ? tiles : num_sms();
+    note_launch();
+    kern<<<grid, THREADS, Cfg<BN>::SMEM, s>>>(ta, tb, M, N, K, ep);
+}
+
+template <int BN>
+void dispatch(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const GemmEpilogue& g,
+              cudaStream_t s) {
+    EpiArgs ep{g.out0, g.ld0, g.n0, g.out1, g.ld1, g.n1, g.out2, g.ld2, g.outf, g.ldf, g.resid, g.ldr};
+    switch (g.kind) {
+        case EPI_QKV: launch_tc<BN, EPI_QKV>(ta, tb, M, N, K, ep, s); break;
+        case EPI_RESID: launch_tc<BN, EPI_RESID>(ta, tb, M, N, K, ep, s); break;
+        case EPI_RELU: launch_tc<BN, EPI_RELU>(ta, tb, M, N, K, ep, s); break;
+        default: launch_tc<BN, EPI_STORE>(ta, tb, M, N, K, ep, s); break;
+    }
+}
+
+}  // namespace
+
+void gemm_bf16_tc(const bf16* A, int64_t M, int64_t K, const bf16* B, int64_t N, const GemmEpilogue& ep,
+                  cudaStream_t s) {
+    if (M <= 0 || N <= 0) return;
+    if (K % 8 != 0 || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15))
+        throw std::runtime_error("gemm_bf16_tc: K must be a multiple of 8 and operands 16-byte aligned");
+    // Wide N keeps the tensor core busy per smem byte; narrow problems use BN=128 so that
+    // more CTAs participate.
+    const int64_t tiles256 = ((M + BM - 1) / BM) * ((N + 255) / 256);
+    const bool wide = N >= 256 && tiles256 >= num_sms() / 2;
+    const int BN = wide ? 256 : 128;
+    CUtensorMap ta, tb;
+    if (!make_tmap_bf16(&ta, A, K, M, K, BK, BM) || !make_tmap_bf16(&tb, B, K, N, K, BK, BN)) {
+        char msg[160];
+        snprintf(msg, sizeof msg, "cuTensorMapEncodeTiled failed (M=%lld N=%lld K=%lld)", (long long)M,
+                 (long long)N, (long long)K);
+        throw std::runtime_error(msg);
+    }
+    if (wide)
+        dispatch<256>(ta, tb, (int)M, (int)N, (int)K, ep, s);
+    else
+        dispatch<128>(ta, tb, (int)M, (int)N, (int)K, ep, s);
+}
+
+}  // namespace kvp

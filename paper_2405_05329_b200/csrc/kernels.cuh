@@ -1,0 +1,87 @@
+// kernels.cuh -- host launchers for the sm_100a kernels of the per-rank layer executor.
+// Every launcher enqueues on the given stream and never synchronises.  Shapes: rows are
+// tokens (token-major, row-major everywhere, like the reference Matrix<T>, matrix.hpp:15).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace kvp {
+
+using bf16 = __nv_bfloat16;
+
+// Counts every kernel launch issued by this library (the bench's gpu_launches claim).
+void note_launch();
+int64_t launch_count();
+
+// ---------------------------------------------------------------- weights.cu
+// Fills a rows x cols matrix from init_weights' SplitMix64 stream (weights.hpp:41-47),
+// value = float((2u - 1) * scale).  f32 variant writes the reference [rows x cols] layout;
+// bf16 variant writes the TRANSPOSED [cols x rows] K-major layout used as the tcgen05 B
+// operand, at row offset `t_row_off` of a packed matrix with leading dimension `ld` (= rows).
+void launch_seeded_f32(float* out, int64_t rows, int64_t cols, double scale, uint64_t stream_seed,
+                       cudaStream_t s);
+void launch_seeded_bf16_t(bf16* out_t, int64_t rows, int64_t cols, double scale, uint64_t stream_seed,
+                          int64_t t_row_off, cudaStream_t s);
+// Host f32 [rows x cols] (already on device) -> bf16 transposed at row offset.
+void launch_transpose_to_bf16(const float* in, int64_t rows, int64_t cols, bf16* out_t, int64_t t_row_off,
+                              cudaStream_t s);
+
+// ---------------------------------------------------------------- norm.cu
+// y = bf16(x * (mean(x^2) + 1e-6)^-1/2) if norm else bf16(x)  (model.hpp:29-45 + cast).
+void launch_norm_cast_bf16(const float* x, bf16* y, int64_t rows, int64_t cols, bool norm, cudaStream_t s);
+// f32 rms_norm_rows with the reference's sequential accumulation order (bit-exact).
+void launch_norm_f32(const float* x, float* y, int64_t rows, int64_t cols, cudaStream_t s);
+void launch_cast_bf16(const float* x, bf16* y, int64_t n, cudaStream_t s);
+void launch_cast_f32(const bf16* x, float* y, int64_t n, cudaStream_t s);
+
+// ---------------------------------------------------------------- gemm_tc.cu
+// D = A[M x K] . B[N x K]^T on tcgen05 (bf16 in, f32 accumulate in TMEM), epilogue fused.
+enum GemmEpi : int {
+    EPI_QKV = 0,    // split bf16 store: cols [0,n0) -> out0, [n0,n0+n1) -> out1, rest -> out2
+    EPI_RESID = 1,  // outf[r, c] = resid[r, c] + acc   (f32, residual stream)
+    EPI_RELU = 2,   // out0[r, c] = bf16(max(acc, 0))
+    EPI_STORE = 3,  // out0[r, c] = bf16(acc)
+};
+struct GemmEpilogue {
+    int kind = EPI_STORE;
+    bf16* out0 = nullptr;
+    int64_t ld0 = 0, n0 = 0;
+    bf16* out1 = nullptr;
+    int64_t ld1 = 0, n1 = 0;
+    bf16* out2 = nullptr;
+    int64_t ld2 = 0;
+    float* outf = nullptr;
+    int64_t ldf = 0;
+    const float* resid = nullptr;
+    int64_t ldr = 0;
+};
+void gemm_bf16_tc(const bf16* A, int64_t M, int64_t K, const bf16* B, int64_t N, const GemmEpilogue& ep,
+                  cudaStream_t s);
+
+// ---------------------------------------------------------------- gemm_simt.cu
+// fp32 parity GEMM: C = A[M x K] . B[K x N] (reference layout), sequential k order with
+// separately rounded multiply and add -> bit-identical to matrix.hpp:76-91.
+enum SimtEpi : int { SEPI_STORE = 0, SEPI_RESID = 1, SEPI_RELU = 2 };
+void gemm_f32_simt(const float* A, int64_t M, int64_t K, int64_t lda, const float* B, int64_t N, float* C,
+                   int64_t ldc, int epi, const float* resid, int64_t ldr, cudaStream_t s);
+
+// ---------------------------------------------------------------- attention
+// Prefix-causal attention (model.hpp:112-158 semantics): query row i (absolute position
+// offset + i) attends keys [0, offset + i].  Q: q_rows x ldq, K/V: k_rows x ldkv (head g
+// at columns [g*hd, (g+1)*hd)), O: q_rows x ldo.  Query head h reads kv head h / group.
+struct AttnShape {
+    int64_t q_rows = 0, k_rows = 0, offset = 0;
+    int n_heads = 1, n_kv_heads = 1, head_dim = 1;
+    int64_t ldq = 0, ldkv = 0, ldo = 0;
+};
+// bf16 tensor-core flash attention (head_dim 64 / 128), tile-skipping, online softmax.
+bool attn_bf16_supported(int head_dim);
+void attn_bf16(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShape& sh, cudaStream_t s);
+// Generic SIMT attention (any head_dim <= 256): f32 math; T = float or bf16 I/O.
+void attn_simt_f32(const float* Q, const float* K, const float* V, float* O, const AttnShape& sh,
+                   cudaStream_t s);
+void attn_simt_bf16(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShape& sh, cudaStream_t s);
+
+}  // namespace kvp
