@@ -11,6 +11,8 @@
 // row's output is bitwise independent of which rank / query tile computes it: Serial, TSP
 // and KVR produce identical bits (the reference's own bit-exactness property,
 // test_engine.cpp:50-88).  Fully masked trailing tiles leave (m, l, O) unchanged exactly.
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace kvp {
@@ -253,7 +255,7 @@ void launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShap
 
 bool attn_bf16_supported(int head_dim) { return head_dim == 64 || head_dim == 128; }
 
-void attn_bf16(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShape& sh, cudaStream_t s) {
+void attn_bf16_mma(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShape& sh, cudaStream_t s) {
     if (sh.q_rows <= 0) return;
     if (sh.head_dim == 128)
         launch<128>(Q, K, V, O, sh, s);
@@ -261,6 +263,18 @@ void attn_bf16(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnS
         launch<64>(Q, K, V, O, sh, s);
     else
         attn_simt_bf16(Q, K, V, O, sh, s);
+}
+
+// tcgen05 kernel by default; KVP_ATTN=mma selects the warp-level mma.sync kernel (A/B runs).
+void attn_bf16(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShape& sh, cudaStream_t s) {
+    static const bool use_mma = [] {
+        const char* e = getenv("KVP_ATTN");
+        return e && e[0] == 'm';
+    }();
+    if (!use_mma && attn_tc_supported(sh.head_dim))
+        attn_bf16_tc(Q, K, V, O, sh, s);
+    else
+        attn_bf16_mma(Q, K, V, O, sh, s);
 }
 
 }  // namespace kvp

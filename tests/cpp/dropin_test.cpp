@@ -1,0 +1,80 @@
+// Drop-in check: reference-style client code (the shapes of test_engine.cpp / acceptance.cpp)
+// compiled against include/kvprefill_b200/kvprefill.hpp and linked to libkvp_b200.so.
+// Exit 0 = all checks passed; prints one line per check.
+#include <cstdio>
+#include <string>
+
+#include "kvprefill_b200/kvprefill.hpp"
+
+using namespace kvprefill;
+
+static int failures = 0;
+static void expect(bool ok, const std::string& what) {
+    std::printf("[%s] %s\n", ok ? "PASS" : "FAIL", what.c_str());
+    if (!ok) ++failures;
+}
+
+int main(int argc, char** argv) {
+    const bool gpu = argc > 1 && std::string(argv[1]) == "--gpu";
+    // host-only parts of the API (no device needed)
+    expect(even_partition(10, 4).sizes() == std::vector<int64_t>({3, 3, 2, 2}), "even_partition(10,4)");
+    expect(partition_from_ratios(10240, {0.35, 0.255, 0.21, 0.185}).sizes() ==
+               std::vector<int64_t>({3584, 2611, 2150, 1895}),
+           "partition_from_ratios golden");
+    bool threw = false;
+    try {
+        even_partition(3, 4);
+    } catch (const PartitionError&) {
+        threw = true;
+    }
+    expect(threw, "PartitionError type preserved across the C-ABI");
+    expect(traffic_pairs(Strategy::KVR, ContextPartition::from_sizes({4, 3, 2})) == 11, "traffic_pairs KVR fixture");
+    ModelConfig sim;
+    sim.n_layers = 32;
+    const auto found = search_partition(16384, 4, sim, CostModel{}, NetworkModel{});
+    expect(found.partition.boundaries == std::vector<int64_t>({0, 6564, 10621, 13754, 16384}), "KVR-S search p=4 16k");
+    if (!gpu) return failures ? 1 : 0;
+
+    // device parts: the reference's accounting fixture and bitwise strategy equivalence
+    ModelConfig mc;
+    mc.d_model = 8;
+    mc.n_heads = 2;
+    mc.n_kv_heads = 2;
+    mc.n_layers = 2;
+    mc.seed = 3;
+    mc.precision = Precision::f32;
+    const auto w = init_weights<float>(mc);
+    const auto ctx = random_context<float>(9, mc.d_model, 21);
+    const auto kvr = run(Strategy::KVR, ctx, ContextPartition::from_sizes({4, 3, 2}), w);
+    expect(kvr.metrics.per_layer_dot_products(0) == 16 && kvr.metrics.per_layer_dot_products(1) == 21 &&
+               kvr.metrics.per_layer_dot_products(2) == 18,
+           "KVR dots 16/21/18");
+    expect(kvr.metrics.per_layer_pairs_sent() == 11 && kvr.metrics.per_layer_rows_sent() == 22 &&
+               kvr.metrics.barrier_count == 0,
+           "KVR 11 pairs / 22 rows / 0 barriers");
+    const auto tsp = run(Strategy::TSP, ctx, even_partition(9, 3), w);
+    expect(tsp.metrics.per_layer_pairs_sent() == 18 && tsp.metrics.barrier_count == mc.n_layers,
+           "TSP 18 pairs / L barriers");
+    const auto serial = run(Strategy::Serial, ctx, even_partition(9, 1), w);
+    expect(serial.hidden_out == kvr.hidden_out && serial.hidden_out == tsp.hidden_out, "Serial == KVR == TSP bitwise");
+    bool proto = false;
+    try {
+        FaultInjection f;
+        f.kind = FaultInjection::Kind::DropMessage;
+        run(Strategy::KVR, ctx, even_partition(9, 3), w, f);
+    } catch (const ProtocolError&) {
+        proto = true;
+    }
+    expect(proto, "dropped handoff -> ProtocolError");
+    mc.precision = Precision::bf16;
+    mc.d_model = 1024;
+    mc.n_heads = 8;
+    mc.n_kv_heads = 8;
+    mc.rms_norm = true;
+    const auto wb = init_weights<float>(mc);
+    const auto big = random_context<float>(512, mc.d_model, 18);
+    const auto a = run(Strategy::KVR, big, partition_from_ratios(512, {0.4, 0.3, 0.2, 0.1}), wb);
+    const auto b = run(Strategy::Serial, big, even_partition(512, 1), wb);
+    expect(a.hidden_out == b.hidden_out, "bf16 tcgen05 path: KVR(p=4) == Serial bitwise");
+    return failures ? 1 : 0;
+}
