@@ -147,6 +147,14 @@ typedef struct kvp_kernel_stats {
 kvp_status kvp_engine_set_profiling(kvp_engine* e, int32_t on);
 kvp_status kvp_engine_kernel_stats(kvp_engine* e, kvp_kernel_stats* out, int32_t max_entries, int32_t* n_out);
 
+/* Calibration for the load balancer: times ONE rank's layer executor in isolation on
+ * devices[0] for `rows` local tokens after a prefix of `offset` tokens (held = offset + rows
+ * keys), median of `reps` runs of layer 0 with synthetic activations.  proj_ms = norm+QKV
+ * GEMM, rest_ms = attention + O-proj + FFN (the terms of CostModel::layer_time,
+ * simnet.hpp:39-43). */
+kvp_status kvp_engine_profile_layer(kvp_engine* e, int64_t rows, int64_t offset, int32_t reps, float* proj_ms,
+                                    float* rest_ms);
+
 /* ------------------------------------------- per-rank layer executor pieces */
 /* layer_qkv (model.hpp:189-192): hidden rows x d -> Q rows x q, K/V rows x kv. */
 kvp_status kvp_layer_qkv(kvp_engine* e, int64_t layer, const float* hidden, int64_t rows, float* Q,

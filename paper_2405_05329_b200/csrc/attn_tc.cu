@@ -1,19 +1,23 @@
 // attn_tc.cu -- prefix-causal flash attention on 5th-gen tensor cores (tcgen05 + TMEM + TMA).
 //
-// Reference: causal_attention (model.hpp:112-158).  One CTA owns a 128-query tile of one head
-// (absolute positions offset + q0 ...) and walks the 128-key tiles [0, offset + last query]:
-//   warp 0      TMA producer: Q once, then K/V tiles through a 2-stage smem ring;
-//   warp 1      MMA issuer (one lane) + TMEM owner:
-//                 S_j = Q K_j^T   (SS: A=Q smem, B=K smem, both K-major SW128) -> TMEM S[j%2]
-//                 O  += P_j V_j   (TS: A=P_j in TMEM, packed bf16 over S[j%2]; B=V smem MN-major)
-//   warps 2..5  softmax, one thread per query row (= TMEM lane): read S_j, mask the diagonal
-//               tile against absolute positions, online softmax in the log2 domain, write
-//               P_j (bf16) back into TMEM; rescale O in TMEM only when a row max grows by
-//               more than 2^8 (exact: l and O always share the same stale max), then the
-//               normalised epilogue O / l -> bf16.
-// TMEM: S0 [0,128) | S1 [128,256) | O [256, 256+hd) of a 512-column allocation.
-// Rows are independent and key tiles are aligned to absolute key 0, so results are bitwise
-// independent of how the context is split over ranks (Serial == TSP == KVR).
+// Reference: causal_attention (model.hpp:112-158).  One CTA owns TWO 128-query tiles (a, b)
+// of one head -- absolute positions offset + q0 ... offset + q0 + 255 -- and walks the
+// 128-key tiles [0, offset + last query]; each K/V tile is loaded once for both query tiles.
+//   warp 0      TMA producer: Q_a, Q_b once, then K/V tiles through a 2-stage smem ring;
+//   warp 1      MMA issuer (one lane) + TMEM owner, ping-pong between the tiles:
+//                 S_x = Q_x K_j^T  (SS: A=Q smem, B=K smem, both K-major SW128) -> TMEM S_x
+//                 O_x += P_x V_j   (TS: A=P_x in TMEM, packed bf16 over S_x; B=V smem MN-major)
+//               so the tensor core works on one tile while the other tile's softmax runs;
+//   warps 2..5  softmax of tile a, warps 6..9 softmax of tile b: one thread per query row
+//               (= TMEM lane), mask of the diagonal tile against absolute positions, online
+//               softmax in the log2 domain with the scale folded into one FFMA per element,
+//               P written back into TMEM as bf16; O is rescaled in TMEM only when a row max
+//               grows by more than 2^8 (exact: l and O always share the same stale max).
+// TMEM: S_a [0,128) | S_b [128,256) | O_a [256, 256+hd) | O_b [384, 384+hd).
+// Key tiles are aligned to absolute key 0, fully masked tiles are skipped per query tile and
+// rows are independent, so results are bitwise independent of how the context is split over
+// ranks (Serial == TSP == KVR).
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 
@@ -27,20 +31,64 @@ bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t 
 
 namespace {
 
-constexpr int BQ = 128;  // queries per CTA
-constexpr int BKV = 128; // keys per tile
-constexpr int THREADS = 192;
+constexpr int BQ = 128;   // queries per tile (two tiles per CTA)
+constexpr int BKV = 128;  // keys per tile
+constexpr int THREADS = 320;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units: p <= 2^8 between rescales
 
 template <int HD>
 struct ACfg {
-    static constexpr int HALVES = HD / 64;                    // 64-wide (128 B) TMA boxes
+    static constexpr int HALVES = HD / 64;  // 64-wide (128 B) TMA boxes
     static constexpr uint32_t Q_BYTES = BQ * HD * 2;
     static constexpr uint32_t KV_BYTES = BKV * HD * 2;
-    static constexpr uint32_t SMEM = Q_BYTES + 4 * KV_BYTES + 1024 + 256;
-    static constexpr uint32_t O_COL = 256;
+    static constexpr uint32_t SMEM = 2 * Q_BYTES + 4 * KV_BYTES + 1024 + 256;
 };
+
+// ---- packed f32x2 arithmetic (sm_100: FFMA2 / FADD2) and exp2 on two pipes ----
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+// MUFU.EX2 (ex2(-inf) = +0 exactly)
+__device__ __forceinline__ float ex2_mufu(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// 2^x on the FMA pipe: x = n + f with n = rint(x) (magic-number add), 2^f by a degree-3
+// minimax polynomial on [-1/2, 1/2] (max rel. error 1.0e-4, far below bf16's 3.9e-3), 2^n
+// added into the exponent bits.  x is clamped at -125 (masked lanes are zeroed by the
+// caller), x <= 8 by the rescale threshold.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    x.x = fmaxf(x.x, -125.f);
+    x.y = fmaxf(x.y, -125.f);
+    const float2 magic = make_float2(12582912.f, 12582912.f), neg1 = make_float2(-1.f, -1.f);
+    const float2 t = fadd2(x, magic);
+    const float2 n = fadd2(t, make_float2(-12582912.f, -12582912.f));
+    const float2 f = ffma2(n, neg1, x);
+    float2 p = ffma2(make_float2(0.055008821f, 0.055008821f), f, make_float2(0.24221078f, 0.24221078f));
+    p = ffma2(p, f, make_float2(0.6932829f, 0.6932829f));
+    p = ffma2(p, f, make_float2(1.f, 1.f));
+    float2 r;
+    r.x = __uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23));
+    r.y = __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23));
+    return r;
+}
 
 struct AttnArgs {
     int64_t q_rows, k_rows, offset;
@@ -50,34 +98,37 @@ struct AttnArgs {
     float sl2;  // softmax scale * log2(e)
 };
 
-template <int HD>
+template <int HD, int POLY_FROM>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
     using C = ACfg<HD>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = smem;
-    uint8_t* sK = sQ + C::Q_BYTES;       // 2 stages
-    uint8_t* sV = sK + 2 * C::KV_BYTES;  // 2 stages
+    uint8_t* sQ = smem;                  // [2] query tiles
+    uint8_t* sK = sQ + 2 * C::Q_BYTES;   // [2] stages
+    uint8_t* sV = sK + 2 * C::KV_BYTES;  // [2] stages
     uint64_t* bar = reinterpret_cast<uint64_t*>(sV + 2 * C::KV_BYTES);
     uint64_t* q_full = bar;
-    uint64_t* k_full = bar + 1;   // [2]
-    uint64_t* v_full = bar + 3;   // [2]
-    uint64_t* kv_empty = bar + 5; // [2]
-    uint64_t* s_full = bar + 7;   // [2]
-    uint64_t* p_full = bar + 9;   // [2]
-    uint64_t* o_done = bar + 11;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+    uint64_t* k_full = bar + 1;    // [2] stages
+    uint64_t* v_full = bar + 3;    // [2] stages
+    uint64_t* kv_empty = bar + 5;  // [2] stages
+    uint64_t* s_full = bar + 7;    // [2] query tiles
+    uint64_t* p_full = bar + 9;    // [2] query tiles
+    uint64_t* o_done = bar + 11;   // [2] query tiles
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int num_qt = static_cast<int>((a.q_rows + BQ - 1) / BQ);
-    const int qt = num_qt - 1 - static_cast<int>(blockIdx.x);  // heaviest tiles first
+    const int num_pairs = static_cast<int>((a.q_rows + 2 * BQ - 1) / (2 * BQ));
+    const int pair = num_pairs - 1 - static_cast<int>(blockIdx.x);  // heaviest first
     const int h = blockIdx.y;
     const int g = h / a.group;
-    const int64_t q0 = static_cast<int64_t>(qt) * BQ;
-    const int64_t last_q = (q0 + BQ - 1 < a.q_rows - 1) ? q0 + BQ - 1 : a.q_rows - 1;
-    const int n_kt = static_cast<int>((a.offset + last_q) / BKV) + 1;
+    const int64_t q0 = static_cast<int64_t>(pair) * 2 * BQ;
+    // key tiles needed by each query tile (tile b covers tile a's range plus one)
+    const int64_t last_a = (q0 + BQ - 1 < a.q_rows - 1) ? q0 + BQ - 1 : a.q_rows - 1;
+    const int64_t last_b = (q0 + 2 * BQ - 1 < a.q_rows - 1) ? q0 + 2 * BQ - 1 : a.q_rows - 1;
+    const int n_kt[2] = {static_cast<int>((a.offset + last_a) / BKV) + 1,
+                         static_cast<int>((a.offset + (last_b > last_a ? last_b : last_a)) / BKV) + 1};
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmQ);
@@ -90,8 +141,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             ptx::mbar_init(&kv_empty[s], 1);
             ptx::mbar_init(&s_full[s], 1);
             ptx::mbar_init(&p_full[s], 4);
+            ptx::mbar_init(&o_done[s], 1);
         }
-        ptx::mbar_init(o_done, 1);
         ptx::fence_barrier_init();
     }
     if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
@@ -102,10 +153,12 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            ptx::mbar_arrive_expect_tx(q_full, C::Q_BYTES);
-            for (int hv = 0; hv < C::HALVES; ++hv)
-                ptx::tma_load_2d(sQ + hv * BQ * 128, &tmQ, q_full, h * HD + hv * 64, static_cast<int32_t>(q0));
-            for (int t = 0; t < n_kt; ++t) {
+            ptx::mbar_arrive_expect_tx(q_full, 2 * C::Q_BYTES);
+            for (int x = 0; x < 2; ++x)
+                for (int hv = 0; hv < C::HALVES; ++hv)
+                    ptx::tma_load_2d(sQ + x * C::Q_BYTES + hv * BQ * 128, &tmQ, q_full, h * HD + hv * 64,
+                                     static_cast<int32_t>(q0 + x * BQ));
+            for (int t = 0; t < n_kt[1]; ++t) {
                 const int s = t & 1;
                 ptx::mbar_wait(&kv_empty[s], ((t >> 1) & 1) ^ 1);
                 ptx::mbar_arrive_expect_tx(&k_full[s], C::KV_BYTES);
@@ -120,120 +173,151 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) {
             constexpr uint32_t idesc_s = ptx::idesc_bf16(BQ, BKV, 0);
             constexpr uint32_t idesc_o = ptx::idesc_bf16(BQ, HD, 1);  // B = V is MN-major
-            const uint32_t q_addr = ptx::smem_u32(sQ);
-            auto issue_s = [&](int t) {
+            auto issue_s = [&](int x, int t) {
                 const int s = t & 1;
                 ptx::mbar_wait(&k_full[s], (t >> 1) & 1);
                 ptx::tc_fence_after();
+                const uint32_t q_addr = ptx::smem_u32(sQ + x * C::Q_BYTES);
                 const uint32_t k_addr = ptx::smem_u32(sK + s * C::KV_BYTES);
 #pragma unroll
                 for (int k = 0; k < HD / 16; ++k) {
                     const uint32_t off = (k >> 2) * (BQ * 128) + (k & 3) * 32;
                     const uint64_t ad = ptx::smem_desc_sw128(q_addr + off, 16, 1024);
                     const uint64_t bd = ptx::smem_desc_sw128(k_addr + (k >> 2) * (BKV * 128) + (k & 3) * 32, 16, 1024);
-                    ptx::mma_bf16_ss(tmem + s * 128, ad, bd, idesc_s, k != 0);
+                    ptx::mma_bf16_ss(tmem + x * 128, ad, bd, idesc_s, k != 0);
                 }
-                ptx::mma_commit(&s_full[s]);
+                ptx::mma_commit(&s_full[x]);
             };
-            ptx::mbar_wait(q_full, 0);
-            issue_s(0);
-            for (int j = 0; j < n_kt; ++j) {
-                const int b = j & 1;
-                if (j + 1 < n_kt) {
-                    if (j >= 1) ptx::mbar_wait(o_done, (j - 1) & 1);  // S[(j+1)%2] held P_{j-1}
-                    issue_s(j + 1);
-                }
-                ptx::mbar_wait(&p_full[b], (j >> 1) & 1);
-                ptx::mbar_wait(&v_full[b], (j >> 1) & 1);
+            auto issue_pv = [&](int x, int t) {
+                const int s = t & 1;
+                ptx::mbar_wait(&p_full[x], t & 1);
+                ptx::mbar_wait(&v_full[s], (t >> 1) & 1);
                 ptx::tc_fence_after();
-                const uint32_t v_addr = ptx::smem_u32(sV + b * C::KV_BYTES);
+                const uint32_t v_addr = ptx::smem_u32(sV + s * C::KV_BYTES);
 #pragma unroll
                 for (int k = 0; k < BKV / 16; ++k) {
                     // B = V[keys 16k..16k+15][hd]: MN-major SW128, LBO = next 64-wide hd block,
                     // SBO = next 8 keys.
                     const uint64_t bd = ptx::smem_desc_sw128(v_addr + k * 16 * 128, BKV * 128, 1024);
-                    ptx::mma_bf16_ts(tmem + C::O_COL, tmem + b * 128 + k * 8, bd, idesc_o, (j | k) != 0);
+                    ptx::mma_bf16_ts(tmem + 256 + x * 128, tmem + x * 128 + k * 8, bd, idesc_o, (t | k) != 0);
                 }
-                ptx::mma_commit(o_done);
-                ptx::mma_commit(&kv_empty[b]);
+                ptx::mma_commit(&o_done[x]);
+            };
+            ptx::mbar_wait(q_full, 0);
+            issue_s(0, 0);
+            issue_s(1, 0);
+            for (int j = 0; j < n_kt[1]; ++j) {
+                if (j < n_kt[0]) {
+                    issue_pv(0, j);
+                    if (j + 1 < n_kt[0]) {
+                        ptx::mbar_wait(&o_done[0], j & 1);  // S_a held P_a(j)
+                        issue_s(0, j + 1);
+                    }
+                }
+                issue_pv(1, j);
+                ptx::mma_commit(&kv_empty[j & 1]);  // tile b is the last reader of stage j%2
+                if (j + 1 < n_kt[1]) {
+                    ptx::mbar_wait(&o_done[1], j & 1);
+                    issue_s(1, j + 1);
+                }
             }
         }
     } else {
-        const uint32_t quarter = warp & 3;
-        const int64_t row = q0 + quarter * 32 + lane;  // local query row
+        const int x = (warp - 2) >> 2;      // query tile of this warpgroup
+        const uint32_t quarter = warp & 3;  // TMEM lane quarter this warp may access
+        const int64_t row = q0 + x * BQ + quarter * 32 + lane;
         const int64_t abs_row = a.offset + row;
         const uint32_t lane_base = tmem + ((quarter * 32u) << 16);
+        const uint32_t s_col = x * 128, o_col = 256 + x * 128;
+        const int nt = n_kt[x];
+        const int64_t tile_first_abs = a.offset + q0 + x * BQ;
         float m_run = -INFINITY, l = 0.f;
-        for (int j = 0; j < n_kt; ++j) {
-            const int b = j & 1;
-            ptx::mbar_wait(&s_full[b], (j >> 1) & 1);
+        for (int j = 0; j < nt; ++j) {
+            ptx::mbar_wait(&s_full[x], j & 1);
             ptx::tc_fence_after();
-            float x[BKV];
+            float sv[BKV];
 #pragma unroll
             for (int c = 0; c < BKV / 32; ++c) {
                 uint32_t r[32];
-                ptx::tmem_ld32(lane_base + b * 128 + c * 32, r);
+                ptx::tmem_ld32(lane_base + s_col + c * 32, r);
                 ptx::tmem_ld_wait();
 #pragma unroll
-                for (int i = 0; i < 32; ++i) x[c * 32 + i] = __uint_as_float(r[i]) * a.sl2;
+                for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(r[i]);
             }
             const int64_t key0 = static_cast<int64_t>(j) * BKV;
-            if (key0 + BKV - 1 > a.offset + q0) {  // tile crosses the causal diagonal
+            if (key0 + BKV - 1 > tile_first_abs) {  // tile crosses the causal diagonal
 #pragma unroll
                 for (int i = 0; i < BKV; ++i)
-                    if (key0 + i > abs_row) x[i] = -INFINITY;
+                    if (key0 + i > abs_row) sv[i] = -INFINITY;
             }
             float mx = -INFINITY;
 #pragma unroll
-            for (int i = 0; i < BKV; ++i) mx = fmaxf(mx, x[i]);
+            for (int i = 0; i < BKV; ++i) mx = fmaxf(mx, sv[i]);
+            mx *= a.sl2;  // scale > 0: max commutes with it
             const bool need = mx > m_run + RESCALE_THRESHOLD;
             if (__any_sync(0xffffffffu, need)) {
                 const float m_new = need ? mx : m_run;
                 const float alpha = need ? exp2f(m_run - m_new) : 1.0f;
                 if (j > 0) {
-                    ptx::mbar_wait(o_done, (j - 1) & 1);
+                    ptx::mbar_wait(&o_done[x], (j - 1) & 1);
                     ptx::tc_fence_after();
 #pragma unroll
                     for (int c = 0; c < HD / 16; ++c) {
                         uint32_t r[16];
-                        ptx::tmem_ld16(lane_base + C::O_COL + c * 16, r);
+                        ptx::tmem_ld16(lane_base + o_col + c * 16, r);
                         ptx::tmem_ld_wait();
 #pragma unroll
                         for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-                        ptx::tmem_st16(lane_base + C::O_COL + c * 16, r);
+                        ptx::tmem_st16(lane_base + o_col + c * 16, r);
                     }
                     ptx::tmem_st_wait();
                 }
                 l *= alpha;
                 m_run = m_new;
             }
-            const float base = (m_run == -INFINITY) ? 0.f : m_run;
+            const float nbv = (m_run == -INFINITY) ? 0.f : -m_run;
+            const float2 sl2v = make_float2(a.sl2, a.sl2), nb2 = make_float2(nbv, nbv);
+            const bool diag = key0 + BKV - 1 > tile_first_abs;  // warp-uniform
+            float2 lacc = make_float2(0.f, 0.f);
 #pragma unroll
             for (int c = 0; c < BKV / 32; ++c) {
                 uint32_t pk[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
-                    const float p0 = exp2f(x[c * 32 + 2 * i] - base);
-                    const float p1 = exp2f(x[c * 32 + 2 * i + 1] - base);
-                    l += p0 + p1;
-                    pk[i] = ptx::pack_bf16(p0, p1);
+                    const int col = c * 32 + 2 * i;
+                    // the exp2 unit is chosen by key column only: deterministic per (row, key)
+                    const float2 xv = ffma2(make_float2(sv[col], sv[col + 1]), sl2v, nb2);
+                    float2 pv;
+                    if (col >= POLY_FROM) {
+                        pv = ex2_poly2(xv);
+                    } else {
+                        pv.x = ex2_mufu(xv.x);
+                        pv.y = ex2_mufu(xv.y);
+                    }
+                    if (diag) {  // masked keys contribute exactly zero
+                        if (key0 + col > abs_row) pv.x = 0.f;
+                        if (key0 + col + 1 > abs_row) pv.y = 0.f;
+                    }
+                    lacc = fadd2(lacc, pv);
+                    pk[i] = ptx::pack_bf16(pv.x, pv.y);
                 }
-                ptx::tmem_st16(lane_base + b * 128 + c * 16, pk);  // P_j over S_j, packed bf16
+                ptx::tmem_st16(lane_base + s_col + c * 16, pk);  // P over S, packed bf16
             }
+            l += lacc.x + lacc.y;
             ptx::tmem_st_wait();
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&p_full[b]);
+            if (lane == 0) ptx::mbar_arrive(&p_full[x]);
         }
         // epilogue: O / l -> bf16
-        ptx::mbar_wait(o_done, (n_kt - 1) & 1);
+        ptx::mbar_wait(&o_done[x], (nt - 1) & 1);
         ptx::tc_fence_after();
         const float inv = 1.0f / l;
         bf16* orow = a.O + row * a.ldo + static_cast<int64_t>(h) * HD;
 #pragma unroll
         for (int c = 0; c < HD / 32; ++c) {
             uint32_t r[32];
-            ptx::tmem_ld32(lane_base + C::O_COL + c * 32, r);
+            ptx::tmem_ld32(lane_base + o_col + c * 32, r);
             ptx::tmem_ld_wait();
             if (row < a.q_rows) {
 #pragma unroll
@@ -256,7 +340,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 }
 
-template <int HD>
+template <int HD, int POLY_FROM>
 void launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShape& sh, cudaStream_t s) {
     CUtensorMap tq, tk, tv;
     if (!make_tmap_bf16(&tq, Q, static_cast<uint64_t>(sh.n_heads) * HD, sh.q_rows, sh.ldq, 64, BQ) ||
@@ -267,14 +351,15 @@ void launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShap
     int dev = 0;
     cudaGetDevice(&dev);
     if (configured != dev) {
-        cudaFuncSetAttribute(attn_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, ACfg<HD>::SMEM);
+        cudaFuncSetAttribute(attn_tc_kernel<HD, POLY_FROM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             ACfg<HD>::SMEM);
         configured = dev;
     }
     AttnArgs a{sh.q_rows, sh.k_rows, sh.offset, sh.n_heads, sh.n_heads / sh.n_kv_heads, sh.ldo, O,
                (1.0f / sqrtf(static_cast<float>(HD))) * 1.4426950408889634f};
-    dim3 grid(static_cast<unsigned>((sh.q_rows + BQ - 1) / BQ), static_cast<unsigned>(sh.n_heads));
+    dim3 grid(static_cast<unsigned>((sh.q_rows + 2 * BQ - 1) / (2 * BQ)), static_cast<unsigned>(sh.n_heads));
     note_launch();
-    attn_tc_kernel<HD><<<grid, THREADS, ACfg<HD>::SMEM, s>>>(tq, tk, tv, a);
+    attn_tc_kernel<HD, POLY_FROM><<<grid, THREADS, ACfg<HD>::SMEM, s>>>(tq, tk, tv, a);
 }
 
 }  // namespace
@@ -283,12 +368,19 @@ bool attn_tc_supported(int head_dim) { return head_dim == 64 || head_dim == 128;
 
 void attn_bf16_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShape& sh, cudaStream_t s) {
     if (sh.q_rows <= 0) return;
-    if (sh.head_dim == 128)
-        launch<128>(Q, K, V, O, sh, s);
-    else if (sh.head_dim == 64)
-        launch<64>(Q, K, V, O, sh, s);
-    else
-        throw std::runtime_error("attn_tc: head_dim must be 64 or 128");
+    // KVP_ATTN_POLY = number of key columns (of 128) whose exp2 runs on the FMA pipe
+    static const int poly = [] {
+        const char* e = getenv("KVP_ATTN_POLY");
+        return e ? atoi(e) : 32;
+    }();
+    if (sh.head_dim != 128 && sh.head_dim != 64) throw std::runtime_error("attn_tc: head_dim must be 64 or 128");
+    const bool h128 = sh.head_dim == 128;
+    switch (poly) {
+        case 0: h128 ? launch<128, 128>(Q, K, V, O, sh, s) : launch<64, 128>(Q, K, V, O, sh, s); break;
+        case 48: h128 ? launch<128, 80>(Q, K, V, O, sh, s) : launch<64, 80>(Q, K, V, O, sh, s); break;
+        case 64: h128 ? launch<128, 64>(Q, K, V, O, sh, s) : launch<64, 64>(Q, K, V, O, sh, s); break;
+        default: h128 ? launch<128, 96>(Q, K, V, O, sh, s) : launch<64, 96>(Q, K, V, O, sh, s); break;
+    }
 }
 
 }  // namespace kvp

@@ -327,7 +327,7 @@ class Fabric {  // Fabric<M> (channel.hpp:103-144)
 struct RankCtx {
     int device = -1;
     cudaStream_t comp = nullptr, comm = nullptr;
-    DevBuf h, h1, x, q, a, mid, kv;
+    DevBuf h, h1, x, q, a, mid, kv, ssq;
     int64_t held = 0;  // rows per layer K (and V) buffer
     std::vector<cudaEvent_t> ev_send, ev_ready, t_start, t_qkv, t_attn, t_end;
     cudaEvent_t ev_begin = nullptr, ev_done = nullptr;
@@ -403,6 +403,7 @@ struct RankCtx {
     }
     ~RankCtx() {
         h.release(); h1.release(); x.release(); q.release(); a.release(); mid.release(); kv.release();
+        ssq.release();
         teardown();
     }
     void alloc(const Shape& s, int64_t rows, int64_t held_rows) {
@@ -413,6 +414,7 @@ struct RankCtx {
         q.ensure(rows * s.q * es, device);
         a.ensure(rows * s.q * es, device);
         mid.ensure(rows * s.f * es, device);
+        ssq.ensure(rows * ssq_parts_for(s.d) * 4, device);
         kv.ensure(static_cast<size_t>(s.L) * 2 * held_rows * s.kv * es, device);
         held = held_rows;
     }
@@ -427,10 +429,16 @@ enum KernelClass { K_NORM = 0, K_GEMM_QKV, K_ATTN, K_GEMM_O, K_GEMM_FFN1, K_GEMM
 static const char* kKernelNames[K_NUM] = {"norm", "gemm_qkv", "attention", "gemm_o", "gemm_ffn1", "gemm_ffn2"};
 
 // layer_qkv (model.hpp:189-192): norm -> fused QKV GEMM; K/V rows land at `kdst`/`vdst`.
-static void exec_qkv(const Shape& s, const LayerW& w, RankCtx& R, int64_t c, void* kdst, void* vdst) {
+static void exec_qkv(const Shape& s, const LayerW& w, RankCtx& R, int64_t c, void* kdst, void* vdst,
+                     bool prep = true) {
     const double gf = 2.0 * c * s.d * (s.q + 2 * s.kv);
     if (s.prec == KVP_BF16) {
-        R.timed(K_NORM, 0, c * s.d * 6.0, [&] { launch_norm_cast_bf16(R.h.as<float>(), R.x.as<bf16>(), c, s.d, s.rms, R.comp); });
+        // x = bf16(h) and its per-128-column sums of squares; from layer 1 on the previous
+        // layer's FFN2 epilogue already produced both (fused RMSNorm).
+        if (prep)
+            R.timed(K_NORM, 0, c * s.d * 6.0, [&] {
+                launch_prep_bf16_ssq(R.h.as<float>(), R.x.as<bf16>(), R.ssq.as<float>(), c, s.d, R.comp);
+            });
         GemmEpilogue ep;
         ep.kind = EPI_QKV;
         ep.out0 = R.q.as<bf16>();
@@ -441,6 +449,11 @@ static void exec_qkv(const Shape& s, const LayerW& w, RankCtx& R, int64_t c, voi
         ep.n1 = s.kv;
         ep.out2 = static_cast<bf16*>(vdst);
         ep.ld2 = s.kv;
+        if (s.rms) {
+            ep.ssq_in = R.ssq.as<float>();
+            ep.ssq_parts = ssq_parts_for(s.d);
+            ep.norm_cols = s.d;
+        }
         R.timed(K_GEMM_QKV, gf, 0, [&] { gemm_bf16_tc(R.x.as<bf16>(), c, s.d, w.wqkv_t, s.q + 2 * s.kv, ep, R.comp); });
     } else {
         const float* x = R.h.as<float>();
@@ -488,13 +501,22 @@ static void exec_finish(const Shape& s, const LayerW& w, RankCtx& R, int64_t c, 
         e1.ldf = s.d;
         e1.resid = R.h.as<float>();
         e1.ldr = s.d;
+        e1.outb = R.x.as<bf16>();  // bf16(h1): the FFN1 A operand
+        e1.ldb = s.d;
+        if (s.rms) {
+            e1.ssq_out = R.ssq.as<float>();
+            e1.ssq_parts = ssq_parts_for(s.d);
+        }
         R.timed(K_GEMM_O, 2.0 * c * s.q * s.d, 0, [&] { gemm_bf16_tc(R.a.as<bf16>(), c, s.q, w.wo_t, s.d, e1, R.comp); });
-        R.timed(K_NORM, 0, c * s.d * 6.0,
-                [&] { launch_norm_cast_bf16(R.h1.as<float>(), R.x.as<bf16>(), c, s.d, s.rms, R.comp); });
         GemmEpilogue e2;
         e2.kind = EPI_RELU;
         e2.out0 = R.mid.as<bf16>();
         e2.ld0 = s.f;
+        if (s.rms) {  // relu(norm(h1).W1) = relu(diag(1/rms).(bf16(h1).W1))
+            e2.ssq_in = R.ssq.as<float>();
+            e2.ssq_parts = ssq_parts_for(s.d);
+            e2.norm_cols = s.d;
+        }
         R.timed(K_GEMM_FFN1, 2.0 * c * s.d * s.f, 0, [&] { gemm_bf16_tc(R.x.as<bf16>(), c, s.d, w.w1_t, s.f, e2, R.comp); });
         GemmEpilogue e3;
         e3.kind = EPI_RESID;
@@ -502,6 +524,12 @@ static void exec_finish(const Shape& s, const LayerW& w, RankCtx& R, int64_t c, 
         e3.ldf = s.d;
         e3.resid = R.h1.as<float>();
         e3.ldr = s.d;
+        e3.outb = R.x.as<bf16>();  // bf16(h): the next layer's QKV A operand
+        e3.ldb = s.d;
+        if (s.rms) {
+            e3.ssq_out = R.ssq.as<float>();
+            e3.ssq_parts = ssq_parts_for(s.d);
+        }
         R.timed(K_GEMM_FFN2, 2.0 * c * s.f * s.d, 0, [&] { gemm_bf16_tc(R.mid.as<bf16>(), c, s.f, w.w2_t, s.d, e3, R.comp); });
     } else {
         R.timed(K_ATTN, af, 0, [&] {
@@ -631,7 +659,7 @@ static void run_engine(kvp_engine* e, int32_t strategy, const float* ctx, int64_
             uint8_t* K = static_cast<uint8_t*>(R.kv_ptr(s, l, 0));
             uint8_t* V = static_cast<uint8_t*>(R.kv_ptr(s, l, 1));
             KVP_CUDA(cudaEventRecord(R.t_start[l], R.comp));
-            exec_qkv(s, w, R, c, K + start * row_kv, V + start * row_kv);
+            exec_qkv(s, w, R, c, K + start * row_kv, V + start * row_kv, l == 0);
             KVP_CUDA(cudaGetLastError());
             KVP_CUDA(cudaEventRecord(R.t_qkv[l], R.comp));
             int64_t k_rows;
@@ -956,6 +984,63 @@ kvp_status kvp_engine_kernel_stats(kvp_engine* e, kvp_kernel_stats* out, int32_t
         const int n = std::min<int>(max_entries, K_NUM);
         for (int k = 0; k < n; ++k) out[k] = acc[k];
         *n_out = n;
+    });
+}
+
+kvp_status kvp_engine_profile_layer(kvp_engine* e, int64_t rows, int64_t offset, int32_t reps, float* proj_ms,
+                                    float* rest_ms) {
+    return guard([&] {
+        if (!e || !proj_ms || !rest_ms) throw Error(KVP_ERR_INPUT, "null argument");
+        if (rows < 1 || offset < 0 || reps < 1) throw Error(KVP_ERR_INPUT, "rows >= 1, offset >= 0, reps >= 1");
+        std::lock_guard<std::mutex> g(e->mu);
+        const Shape& s = e->s;
+        const LayerW& w = layer_of(e, 0, 0);
+        const int64_t held = offset + rows;
+        RankCtx& R = util_ctx(e, rows, held);
+        KVP_CUDA(cudaSetDevice(R.device));
+        // synthetic activations: a seeded uniform context and a seeded prefix cache
+        launch_seeded_f32(R.h.as<float>(), rows, s.d, 1.0, 0x5eedull, R.comp);
+        if (s.prec == KVP_BF16) {
+            DevBuf tmp;
+            tmp.ensure(held * s.kv * 4, R.device);
+            for (int which = 0; which < 2; ++which) {
+                launch_seeded_f32(tmp.as<float>(), held, s.kv, 1.0, 0x5eed1ull + which, R.comp);
+                launch_cast_bf16(tmp.as<float>(), static_cast<bf16*>(R.kv_ptr(s, 0, which)), held * s.kv, R.comp);
+            }
+            KVP_CUDA(cudaStreamSynchronize(R.comp));
+        } else {
+            for (int which = 0; which < 2; ++which)
+                launch_seeded_f32(static_cast<float*>(R.kv_ptr(s, 0, which)), held, s.kv, 1.0, 0x5eed1ull + which, R.comp);
+        }
+        cudaEvent_t ev[3];
+        for (auto& x : ev) KVP_CUDA(cudaEventCreate(&x));
+        std::vector<float> pa, ra;
+        uint8_t* K = static_cast<uint8_t*>(R.kv_ptr(s, 0, 0));
+        uint8_t* V = static_cast<uint8_t*>(R.kv_ptr(s, 0, 1));
+        const size_t row_kv = static_cast<size_t>(s.kv) * s.es();
+        const bool prof = R.profiling;
+        R.profiling = false;
+        for (int i = 0; i < reps + 1; ++i) {
+            KVP_CUDA(cudaEventRecord(ev[0], R.comp));
+            exec_qkv(s, w, R, rows, K + offset * row_kv, V + offset * row_kv, true);
+            KVP_CUDA(cudaEventRecord(ev[1], R.comp));
+            exec_finish(s, w, R, rows, K, V, held, offset);
+            KVP_CUDA(cudaEventRecord(ev[2], R.comp));
+            KVP_CUDA(cudaEventSynchronize(ev[2]));
+            float a = 0, b = 0;
+            KVP_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
+            KVP_CUDA(cudaEventElapsedTime(&b, ev[1], ev[2]));
+            if (i > 0) {  // first run warms up
+                pa.push_back(a);
+                ra.push_back(b);
+            }
+        }
+        R.profiling = prof;
+        for (auto& x : ev) cudaEventDestroy(x);
+        std::sort(pa.begin(), pa.end());
+        std::sort(ra.begin(), ra.end());
+        *proj_ms = pa[pa.size() / 2];
+        *rest_ms = ra[ra.size() / 2];
     });
 }
 

@@ -16,6 +16,7 @@
 // Operand tails (M, N, K not multiples of the tile) are zero-filled by TMA; the epilogue
 // predicates rows and columns.
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 
@@ -92,28 +93,57 @@ struct EpiArgs {
     int64_t ldf;
     const float* resid;
     int64_t ldr;
+    bf16* outb;
+    int64_t ldb;
+    float* ssq_out;
+    const float* ssq_in;
+    int ssq_parts;
+    float inv_norm_cols;
 };
 
+// Returns the sum of squares of the stored values (EPI_RESID; feeds the fused RMSNorm).
 template <int KIND>
-__device__ __forceinline__ void store_chunk(const EpiArgs& ep, int64_t row, int64_t col0, int64_t N,
-                                            const uint32_t (&r)[32]) {
+__device__ __forceinline__ float store_chunk(const EpiArgs& ep, int64_t row, int64_t col0, int64_t N,
+                                             const uint32_t (&r)[32], float row_scale) {
     const bool full = col0 + 32 <= N;
+    float ss = 0.f;
     if constexpr (KIND == EPI_RESID) {
         float* o = ep.outf + row * ep.ldf + col0;
         const float* rs = ep.resid + row * ep.ldr + col0;
+        bf16* ob = ep.outb ? ep.outb + row * ep.ldb + col0 : nullptr;
         if (full) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
+            for (int j = 0; j < 32; j += 8) {
                 const float4 a = *reinterpret_cast<const float4*>(rs + j);
-                float4 v;
+                const float4 b = *reinterpret_cast<const float4*>(rs + j + 4);
+                float4 v, w;
                 v.x = a.x + __uint_as_float(r[j + 0]);
                 v.y = a.y + __uint_as_float(r[j + 1]);
                 v.z = a.z + __uint_as_float(r[j + 2]);
                 v.w = a.w + __uint_as_float(r[j + 3]);
+                w.x = b.x + __uint_as_float(r[j + 4]);
+                w.y = b.y + __uint_as_float(r[j + 5]);
+                w.z = b.z + __uint_as_float(r[j + 6]);
+                w.w = b.w + __uint_as_float(r[j + 7]);
                 *reinterpret_cast<float4*>(o + j) = v;
+                *reinterpret_cast<float4*>(o + j + 4) = w;
+                ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w + w.x * w.x + w.y * w.y + w.z * w.z + w.w * w.w;
+                if (ob) {
+                    uint4 pk;
+                    pk.x = ptx::pack_bf16(v.x, v.y);
+                    pk.y = ptx::pack_bf16(v.z, v.w);
+                    pk.z = ptx::pack_bf16(w.x, w.y);
+                    pk.w = ptx::pack_bf16(w.z, w.w);
+                    *reinterpret_cast<uint4*>(ob + j) = pk;
+                }
             }
         } else {
-            for (int j = 0; j < 32 && col0 + j < N; ++j) o[j] = rs[j] + __uint_as_float(r[j]);
+            for (int j = 0; j < 32 && col0 + j < N; ++j) {
+                const float v = rs[j] + __uint_as_float(r[j]);
+                o[j] = v;
+                ss += v * v;
+                if (ob) ob[j] = __float2bfloat16_rn(v);
+            }
         }
     } else {
         bf16* o;
@@ -126,9 +156,9 @@ __device__ __forceinline__ void store_chunk(const EpiArgs& ep, int64_t row, int6
                     const int64_t c = col0 + j;
                     bf16* dst = c < e0 ? ep.out0 + row * ep.ld0 + c
                                        : (c < e1 ? ep.out1 + row * ep.ld1 + (c - e0) : ep.out2 + row * ep.ld2 + (c - e1));
-                    *dst = __float2bfloat16_rn(__uint_as_float(r[j]));
+                    *dst = __float2bfloat16_rn(__uint_as_float(r[j]) * row_scale);
                 }
-                return;
+                return 0.f;
             }
             if (col0 < ep.n0) {
                 o = ep.out0 + row * ep.ld0 + col0;
@@ -143,7 +173,7 @@ __device__ __forceinline__ void store_chunk(const EpiArgs& ep, int64_t row, int6
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-            v[j] = __uint_as_float(r[j]);
+            v[j] = __uint_as_float(r[j]) * row_scale;
             if constexpr (KIND == EPI_RELU) v[j] = v[j] < 0.f ? 0.f : v[j];
         }
         if (full) {
@@ -160,6 +190,7 @@ __device__ __forceinline__ void store_chunk(const EpiArgs& ep, int64_t row, int6
             for (int j = 0; j < 32 && col0 + j < N; ++j) o[j] = __float2bfloat16_rn(v[j]);
         }
     }
+    return ss;
 }
 
 template <int BN, int KIND>
@@ -261,6 +292,16 @@ __global__ void __launch_bounds__(THREADS, 1)
             ptx::tc_fence_after();
             const int64_t row = static_cast<int64_t>(m_blk) * BM + quarter * 32 + lane;
             const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + buf * BN;
+            float row_scale = 1.f;
+            if constexpr (KIND != EPI_RESID) {
+                if (ep.ssq_in != nullptr && row < M) {
+                    const float* sp = ep.ssq_in + row * ep.ssq_parts;
+                    float ss = 0.f;
+                    for (int q = 0; q < ep.ssq_parts; ++q) ss += sp[q];
+                    row_scale = 1.0f / sqrtf(ss * ep.inv_norm_cols + 1e-6f);
+                }
+            }
+            float ssacc = 0.f;
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 const int64_t col0 = static_cast<int64_t>(n_blk) * BN + c * 32;
@@ -268,7 +309,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                 uint32_t r[32];
                 ptx::tmem_ld32(taddr + c * 32, r);
                 ptx::tmem_ld_wait();
-                if (row < M) store_chunk<KIND>(ep, row, col0, N, r);
+                if (row < M) ssacc += store_chunk<KIND>(ep, row, col0, N, r, row_scale);
+                if constexpr (KIND == EPI_RESID) {
+                    // one partial per 128-column group, independent of BN (deterministic)
+                    if (ep.ssq_out != nullptr && row < M && (((c + 1) & 3) == 0 || col0 + 32 >= N)) {
+                        ep.ssq_out[row * ep.ssq_parts + (col0 >> 7)] = ssacc;
+                        ssacc = 0.f;
+                    }
+                }
             }
             ptx::tc_fence_before();
             __syncwarp();
@@ -303,7 +351,8 @@ void launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K
 template <int BN>
 void dispatch(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const GemmEpilogue& g,
               cudaStream_t s) {
-    EpiArgs ep{g.out0, g.ld0, g.n0, g.out1, g.ld1, g.n1, g.out2, g.ld2, g.outf, g.ldf, g.resid, g.ldr};
+    EpiArgs ep{g.out0, g.ld0, g.n0, g.out1, g.ld1, g.n1, g.out2, g.ld2, g.outf, g.ldf, g.resid, g.ldr,
+               g.outb, g.ldb, g.ssq_out, g.ssq_in, g.ssq_parts, g.norm_cols ? 1.0f / static_cast<float>(g.norm_cols) : 0.f};
     switch (g.kind) {
         case EPI_QKV: launch_tc<BN, EPI_QKV>(ta, tb, M, N, K, ep, s); break;
         case EPI_RESID: launch_tc<BN, EPI_RESID>(ta, tb, M, N, K, ep, s); break;
@@ -319,10 +368,25 @@ void gemm_bf16_tc(const bf16* A, int64_t M, int64_t K, const bf16* B, int64_t N,
     if (M <= 0 || N <= 0) return;
     if (K % 8 != 0 || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15))
         throw std::runtime_error("gemm_bf16_tc: K must be a multiple of 8 and operands 16-byte aligned");
-    // Wide N keeps the tensor core busy per smem byte; narrow problems use BN=128 so that
-    // more CTAs participate.
-    const int64_t tiles256 = ((M + BM - 1) / BM) * ((N + 255) / 256);
-    const bool wide = N >= 256 && tiles256 >= num_sms() / 2;
+    // Tile width: BN=256 feeds the tensor core with the least smem traffic per FLOP; BN=128
+    // halves the tile so the persistent grid quantises better (e.g. 4096x4096 outputs are 512
+    // tiles = 3.46 waves of 148 SMs at BN=256 but 6.92 waves at BN=128).  Pick the width with
+    // the best (wave efficiency x per-tile efficiency); KVP_GEMM_BN=128|256 forces one.
+    static const int forced = [] {
+        const char* e = getenv("KVP_GEMM_BN");
+        return e ? atoi(e) : 0;
+    }();
+    const int sms = num_sms();
+    auto score = [&](int64_t bn, double tile_eff) {
+        const int64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+        const int64_t waves = (tiles + sms - 1) / sms;
+        const double useful = static_cast<double>(M) * N / (static_cast<double>(waves) * sms * BM * bn);
+        return useful * tile_eff;
+    };
+    bool wide = score(256, 1.0) >= score(128, 0.72);  // BN=128 tiles measured ~25% slower per FLOP
+    if (N < 256) wide = false;
+    if (forced == 128) wide = false;
+    if (forced == 256 && N >= 256) wide = true;
     const int BN = wide ? 256 : 128;
     CUtensorMap ta, tb;
     if (!make_tmap_bf16(&ta, A, K, M, K, BK, BM) || !make_tmap_bf16(&tb, B, K, N, K, BK, BN)) {

@@ -112,6 +112,8 @@ _SIGS = {
     "kvp_engine_last_launch_count": (C.c_int, [_P, _I64P]),
     "kvp_engine_set_profiling": (C.c_int, [_P, C.c_int32]),
     "kvp_engine_kernel_stats": (C.c_int, [_P, C.POINTER(_KStats), C.c_int32, C.POINTER(C.c_int32)]),
+    "kvp_engine_profile_layer": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, C.POINTER(C.c_float),
+                                           C.POINTER(C.c_float)]),
     "kvp_layer_qkv": (C.c_int, [_P, C.c_int64, _P, C.c_int64, _P, _P, _P]),
     "kvp_causal_attention": (C.c_int, [_P, _P, C.c_int64, _P, _P, C.c_int64, C.c_int64, _P]),
     "kvp_layer_finish": (C.c_int, [_P, C.c_int64, _P, C.c_int64, _P, _P, _P, C.c_int64, C.c_int64, _P]),
@@ -388,6 +390,12 @@ class WeightSet:
         return {arr[i].name.decode(): {"launches": arr[i].launches, "total_ms": arr[i].total_ms,
                                        "flops": arr[i].flops, "bytes": arr[i].bytes} for i in range(n.value)}
 
+    def profile_layer(self, rows: int, offset: int, reps: int = 5):
+        """(proj_ms, rest_ms): one rank's layer executor timed in isolation (CUDA events)."""
+        a, b = C.c_float(), C.c_float()
+        _check(lib().kvp_engine_profile_layer(self._h, rows, offset, reps, C.byref(a), C.byref(b)), "profile_layer")
+        return float(a.value), float(b.value)
+
     def last_launch_count(self) -> int:
         v = C.c_int64()
         _check(lib().kvp_engine_last_launch_count(self._h, C.byref(v)), "last_launch_count")
@@ -629,6 +637,25 @@ def fit_cost_model(local_rows, held_rows, proj_s, rest_s) -> CostModel:
     out = _Cost()
     _check(lib().kvp_fit_cost_model(_vp(a), _vp(b), _vp(c), _vp(d), len(a), C.byref(out)), "fit_cost_model")
     return CostModel(out.alpha, out.proj_coeff, out.softmax_coeff, out.fixed_overhead)
+
+
+def calibrate_cost_model(weights: WeightSet, C_: int, p: int, reps: int = 3) -> CostModel:
+    """Fits the balancer's CostModel to MEASURED B200 layer times: one rank's layer executor is
+    timed in isolation on a grid of (local rows, prefix) points that spans the partitions
+    the search will visit at (C, p), then kvp_fit_cost_model solves proj ~ a*c and
+    rest ~ alpha*c*held + s*c + f.  Times are per layer; simulate_ttft multiplies by L."""
+    rows, held, proj, rest = [], [], [], []
+    for frac in (0.5, 1.0, 1.5):
+        c = max(1, int(round(frac * C_ / p)))
+        for b in sorted({0, C_ // 4, C_ // 2, (3 * C_) // 4}):
+            if b + c > C_:
+                continue
+            pm, rm = weights.profile_layer(c, b, reps)
+            rows.append(c)
+            held.append(b + c)
+            proj.append(pm * 1e-3)
+            rest.append(rm * 1e-3)
+    return fit_cost_model(rows, held, proj, rest)
 
 
 def max_rel_dev(a, b) -> float:
