@@ -9,9 +9,9 @@ A "step" is one prompt phase (all 32 layers, first-token readout) over one synth
 HBM; `e2e` = the same through the public API (kvprefill.run) from pinned host memory, H2D of
 the context and D2H of the first-token row inside the timed region.  One JSON line on rank 0.
 
-N>1 (torchrun, one process per GPU): rank 0 drives an engine over all N local GPUs (one host
-thread + streams per GPU, KV handoff by peer copies over NVLink); the other ranks join the
-barriers.  The NCCL multi-process transport is the next step.
+N>1 (torchrun, one process per GPU): every rank drives its own B200 layer executor through
+the kvp_rank_* C-ABI and the KV-Runahead handoff (or the TSP all-gather) moves over NCCL
+(NVLink) via paper_2405_05329_b200.distributed; TTFT = max over ranks of the device time.
 """
 from __future__ import annotations
 
@@ -210,6 +210,102 @@ def run_reference_arm(args, w, rank, world):
 
 
 # ------------------------------------------------------------------ our arm
+def run_multi(args, w, rank, world, local):
+    """One process per GPU: KVR chain / TSP all-gather over NCCL through the distributed driver."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_05329_b200 import kvprefill as kv
+    from paper_2405_05329_b200.distributed import GpuExecutor, Transport, run_rank
+
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    C = w["C"]
+    cfg = kv.ModelConfig(w["d_model"], w["n_heads"], w["n_kv_heads"], w["n_layers"], 1, "bf16", w["rms_norm"])
+    W = kv.init_weights(cfg, [local])
+    strategy = kv.Strategy.KVR if args.strategy == "kvr" else kv.Strategy.TSP
+    part = kv.even_partition(C, world)
+    if args.partition == "search" and strategy == kv.Strategy.KVR:
+        # KVR-S: the reference's grid search on a CostModel calibrated from measured B200 layer
+        # times (rank 0), broadcast to every rank
+        obj = [None]
+        if rank == 0:
+            cost = kv.calibrate_cost_model(W, C, world)
+            kv_dim = w["n_kv_heads"] * (w["d_model"] // w["n_heads"])
+            net = kv.NetworkModel(bandwidth=770e9 / (2 * kv_dim * 2), latency=10e-6)
+            obj = [kv.search_partition(C, world, cfg, cost, net).partition.boundaries]
+        dist.broadcast_object_list(obj, src=0)
+        part = kv.ContextPartition(C, obj[0])
+    b = part.boundaries
+    rows_np = np.random.default_rng(18).uniform(-1.0, 1.0, (C, w["d_model"])).astype(np.float32)[b[rank]:b[rank + 1]]
+    rows_host = torch.from_numpy(rows_np).pin_memory()
+    rows_dev = rows_host.to(f"cuda:{local}")
+    ex = GpuExecutor(W, local)
+    tr = Transport()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def step(rows):
+        flush.zero_()
+        torch.cuda.synchronize()
+        dist.barrier()
+        return run_rank(strategy, rows, part, ex, tr, rank, world, w["n_layers"])
+
+    for _ in range(args.warmup):
+        step(rows_dev)
+    dist.barrier()
+    torch.cuda.synchronize()
+    times = []
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            times.append(step(rows_dev).ttft_ms)
+        torch.cuda.synchronize()
+        dist.barrier()
+        wall = time.perf_counter() - t0
+    ms = statistics.mean(times)
+    W.set_profiling(True)
+    step(rows_dev)
+    stats = W.kernel_stats()
+    W.set_profiling(False)
+    e2e_t = []
+    if not args.no_e2e:
+        for i in range(args.warmup + args.steps):
+            r = step(rows_host.numpy())
+            if i >= args.warmup:
+                e2e_t.append(r.ttft_ms)
+    clocks = [None] * world
+    dist.all_gather_object(clocks, clk.summary())
+    if rank == 0:
+        peaks = load_peaks()
+        gemm = [v for k, v in stats.items() if k.startswith("gemm")]
+        g_ms = sum(v["total_ms"] for v in gemm)
+        g_fl = sum(v["flops"] for v in gemm)
+        achieved = g_fl / (g_ms * 1e-3) / 1e12 if g_ms else 0.0
+        F = algorithmic_flops(w, C)
+        line = {"metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded init_weights + uniform context)",
+                "config": {"workload": args.workload, **w, "strategy": args.strategy, "partition": b,
+                           "ranks": world, "transport": "nccl p2p (kvr) / batched p2p all-gather (tsp)",
+                           "l2": "flushed (256 MB write) before every step",
+                           "parallelism": f"{args.strategy}-p{world}"},
+                "ttft_roofline_frac": (F / (world * peaks["bf16"] * 1e12)) / (ms * 1e-3),
+                "algorithmic_tflop": F / 1e12, "wall_s_timed": wall,
+                "roofline": {"bound": "tensor", "kernel": "gemm_bf16_tc (rank 0)", "achieved": achieved,
+                             "peak": peaks["bf16_sustained"], "unit": "TFLOP/s",
+                             "frac": achieved / peaks["bf16_sustained"], "traffic": None},
+                "kernels_rank0": {k: {"launches": v["launches"], "ms": round(v["total_ms"], 4)} for k, v in stats.items()},
+                "clocks": clocks[0], "clocks_all": clocks,
+                "gpu_launches": None,
+                "e2e": {"value": statistics.mean(e2e_t), "unit": "ms", "h2d_bytes_per_step": C * w["d_model"] * 4,
+                        "d2h_bytes_per_step": C * w["d_model"] * 4} if e2e_t else None}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    W.close()
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -218,6 +314,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="llama7b-4k", choices=sorted(WORKLOADS))
     ap.add_argument("--strategy", default="kvr", choices=["kvr", "tsp"])
+    ap.add_argument("--partition", default="even", choices=["even", "search"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -239,17 +336,8 @@ def main():
     from paper_2405_05329_b200 import kvprefill as kv
 
     if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    n = args.gpus if world == 1 else world
-    if rank != 0:  # rank 0 drives the engine over all local GPUs (see module doc)
-        for _ in range(4):
-            barrier(world)
-        import torch.distributed as dist
-        dist.destroy_process_group()
-        return 0
-
+        return run_multi(args, w, rank, world, local)
+    n = args.gpus
     C = w["C"]
     cfg = kv.ModelConfig(w["d_model"], w["n_heads"], w["n_kv_heads"], w["n_layers"], 1, "bf16", w["rms_norm"])
     devices = list(range(n))
@@ -274,7 +362,6 @@ def main():
 
     for _ in range(args.warmup):
         step_device()
-    barrier(world)
     torch.cuda.synchronize()
     times, launches = [], 0
     with ClockSampler(0) as clk:
@@ -285,7 +372,6 @@ def main():
             launches += nl
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
-    barrier(world)
     ms = statistics.mean(times)
 
     # profiled pass: per-kernel-class device time (events on the launching stream)
@@ -352,11 +438,6 @@ def main():
             line["cpu_baseline"] = {"value": None, "error": str(ex)}
     print(json.dumps(line), flush=True)
     W.close()
-    if world > 1:
-        for _ in range(2):
-            barrier(world)
-        import torch.distributed as dist
-        dist.destroy_process_group()
     return 0
 
 

@@ -155,6 +155,28 @@ kvp_status kvp_engine_kernel_stats(kvp_engine* e, kvp_kernel_stats* out, int32_t
 kvp_status kvp_engine_profile_layer(kvp_engine* e, int64_t rows, int64_t offset, int32_t reps, float* proj_ms,
                                     float* rest_ms);
 
+/* ------------------------------------------- one rank of a multi-process run */
+/* One process per GPU: the caller owns the transport (e.g. NCCL p2p via torch.distributed)
+ * and drives one rank's per-layer schedule -- the worker loop of run<T>
+ * (engine.hpp:223-296) with the Channel send/recv replaced by the caller's transport.
+ * kv_bufs: 2*n_layers device pointers (K_0, V_0, K_1, V_1, ...), each [held x kv] in the
+ * engine's element type (bf16 or f32), owned by the caller (so the transport can address
+ * them); NULL = engine-owned buffers.  rows: the rank's context rows [start, start+n_rows)
+ * (host f32, or device f32 when rows_on_device).  Work is enqueued on the engine stream
+ * returned by kvp_rank_stream; the caller orders its transport on that stream. */
+kvp_status kvp_rank_begin(kvp_engine* e, const float* rows, int64_t n_rows, int64_t start, int64_t held,
+                          int32_t rows_on_device, void* const* kv_bufs);
+kvp_status kvp_rank_stream(kvp_engine* e, void** stream);
+kvp_status kvp_rank_kv(kvp_engine* e, int64_t layer, void** K, void** V);
+/* layer_qkv for the local rows: K/V rows land at [start, start+n_rows) of layer `layer`. */
+kvp_status kvp_rank_qkv(kvp_engine* e, int64_t layer);
+/* layer_finish over keys [0, k_rows) of layer `layer` with mask offset = start. */
+kvp_status kvp_rank_finish(kvp_engine* e, int64_t layer, int64_t k_rows);
+/* Synchronises, writes the final hidden rows (n_rows x d; host or device per out_on_device,
+ * nullable) and the last local row (d floats, host, nullable); *ms = device time of the rank
+ * from kvp_rank_begin to the last layer (nullable). */
+kvp_status kvp_rank_end(kvp_engine* e, float* out_rows, int32_t out_on_device, float* last_row, float* ms);
+
 /* ------------------------------------------- per-rank layer executor pieces */
 /* layer_qkv (model.hpp:189-192): hidden rows x d -> Q rows x q, K/V rows x kv. */
 kvp_status kvp_layer_qkv(kvp_engine* e, int64_t layer, const float* hidden, int64_t rows, float* Q,

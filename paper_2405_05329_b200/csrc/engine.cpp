@@ -329,6 +329,7 @@ struct RankCtx {
     cudaStream_t comp = nullptr, comm = nullptr;
     DevBuf h, h1, x, q, a, mid, kv, ssq;
     int64_t held = 0;  // rows per layer K (and V) buffer
+    std::vector<void*> ext_kv;  // caller-owned per-layer K/V buffers (multi-process mode)
     std::vector<cudaEvent_t> ev_send, ev_ready, t_start, t_qkv, t_attn, t_end;
     cudaEvent_t ev_begin = nullptr, ev_done = nullptr;
     // profiling: (class, flops, bytes, start event, end event) per launch
@@ -406,8 +407,9 @@ struct RankCtx {
         ssq.release();
         teardown();
     }
-    void alloc(const Shape& s, int64_t rows, int64_t held_rows) {
+    void alloc(const Shape& s, int64_t rows, int64_t held_rows, bool own_kv = true) {
         const size_t es = s.es();
+        if (own_kv) ext_kv.clear();
         h.ensure(rows * s.d * 4, device);
         h1.ensure(rows * s.d * 4, device);
         x.ensure(rows * s.d * es, device);
@@ -415,11 +417,12 @@ struct RankCtx {
         a.ensure(rows * s.q * es, device);
         mid.ensure(rows * s.f * es, device);
         ssq.ensure(rows * ssq_parts_for(s.d) * 4, device);
-        kv.ensure(static_cast<size_t>(s.L) * 2 * held_rows * s.kv * es, device);
+        if (own_kv) kv.ensure(static_cast<size_t>(s.L) * 2 * held_rows * s.kv * es, device);
         held = held_rows;
     }
     // K or V of layer l: [held x kv], element size es.
     void* kv_ptr(const Shape& s, int64_t l, int which) const {
+        if (!ext_kv.empty()) return ext_kv[static_cast<size_t>(2 * l + which)];
         return kv.as<uint8_t>() + ((2 * l + which) * held * s.kv) * s.es();
     }
 };
@@ -573,6 +576,9 @@ struct kvp_engine {
     float last_ttft = 0.f;
     int64_t last_launches = 0;
     bool profiling = false;
+    // multi-process rank session
+    bool in_session = false;
+    int64_t sess_rows = 0, sess_start = 0;
 };
 
 namespace kvp {
@@ -1041,6 +1047,109 @@ kvp_status kvp_engine_profile_layer(kvp_engine* e, int64_t rows, int64_t offset,
         std::sort(ra.begin(), ra.end());
         *proj_ms = pa[pa.size() / 2];
         *rest_ms = ra[ra.size() / 2];
+    });
+}
+
+kvp_status kvp_rank_begin(kvp_engine* e, const float* rows, int64_t n_rows, int64_t start, int64_t held,
+                          int32_t rows_on_device, void* const* kv_bufs) {
+    return guard([&] {
+        if (!e || !rows) throw Error(KVP_ERR_INPUT, "null argument");
+        if (n_rows < 1 || start < 0 || held < start + n_rows)
+            throw Error(KVP_ERR_CACHE, "rank session needs n_rows >= 1 and held >= start + n_rows");
+        std::lock_guard<std::mutex> g(e->mu);
+        const Shape& s = e->s;
+        if (e->ranks.empty()) e->ranks.push_back(std::make_unique<RankCtx>());
+        RankCtx& R = *e->ranks[0];
+        R.setup(e->devices[0], s.L);
+        R.alloc(s, n_rows, held, kv_bufs == nullptr);
+        if (kv_bufs) R.ext_kv.assign(kv_bufs, kv_bufs + 2 * s.L);
+        R.profiling = e->profiling;
+        R.marks.clear();
+        R.pool_used = 0;
+        KVP_CUDA(cudaSetDevice(R.device));
+        KVP_CUDA(cudaEventRecord(R.ev_begin, R.comp));
+        KVP_CUDA(cudaMemcpyAsync(R.h.p, rows, n_rows * s.d * 4, rows_on_device ? cudaMemcpyDeviceToDevice
+                                                                                 : cudaMemcpyHostToDevice, R.comp));
+        e->in_session = true;
+        e->sess_rows = n_rows;
+        e->sess_start = start;
+        e->last_p = 1;
+    });
+}
+
+static RankCtx& session_rank(kvp_engine* e) {
+    if (!e || !e->in_session) throw Error(KVP_ERR_INPUT, "no rank session (call kvp_rank_begin)");
+    RankCtx& R = *e->ranks[0];
+    KVP_CUDA(cudaSetDevice(R.device));
+    return R;
+}
+
+kvp_status kvp_rank_stream(kvp_engine* e, void** stream) {
+    return guard([&] {
+        std::lock_guard<std::mutex> g(e->mu);
+        *stream = session_rank(e).comp;
+    });
+}
+
+kvp_status kvp_rank_kv(kvp_engine* e, int64_t layer, void** K, void** V) {
+    return guard([&] {
+        std::lock_guard<std::mutex> g(e->mu);
+        RankCtx& R = session_rank(e);
+        if (layer < 0 || layer >= e->s.L) throw Error(KVP_ERR_DIMENSION, "layer index out of range");
+        *K = R.kv_ptr(e->s, layer, 0);
+        *V = R.kv_ptr(e->s, layer, 1);
+    });
+}
+
+kvp_status kvp_rank_qkv(kvp_engine* e, int64_t layer) {
+    return guard([&] {
+        std::lock_guard<std::mutex> g(e->mu);
+        RankCtx& R = session_rank(e);
+        const Shape& s = e->s;
+        const LayerW& w = layer_of(e, 0, layer);
+        const size_t row_kv = static_cast<size_t>(s.kv) * s.es();
+        uint8_t* K = static_cast<uint8_t*>(R.kv_ptr(s, layer, 0));
+        uint8_t* V = static_cast<uint8_t*>(R.kv_ptr(s, layer, 1));
+        KVP_CUDA(cudaEventRecord(R.t_start[layer], R.comp));
+        exec_qkv(s, w, R, e->sess_rows, K + e->sess_start * row_kv, V + e->sess_start * row_kv, layer == 0);
+        KVP_CUDA(cudaGetLastError());
+        KVP_CUDA(cudaEventRecord(R.t_qkv[layer], R.comp));
+    });
+}
+
+kvp_status kvp_rank_finish(kvp_engine* e, int64_t layer, int64_t k_rows) {
+    return guard([&] {
+        std::lock_guard<std::mutex> g(e->mu);
+        RankCtx& R = session_rank(e);
+        const Shape& s = e->s;
+        const LayerW& w = layer_of(e, 0, layer);
+        if (k_rows < e->sess_start + e->sess_rows || k_rows > R.held)
+            throw Error(KVP_ERR_CACHE, "finish needs sess_start + rows <= k_rows <= held");
+        KVP_CUDA(cudaEventRecord(R.t_attn[layer], R.comp));
+        exec_finish(s, w, R, e->sess_rows, R.kv_ptr(s, layer, 0), R.kv_ptr(s, layer, 1), k_rows, e->sess_start);
+        KVP_CUDA(cudaGetLastError());
+        KVP_CUDA(cudaEventRecord(R.t_end[layer], R.comp));
+    });
+}
+
+kvp_status kvp_rank_end(kvp_engine* e, float* out_rows, int32_t out_on_device, float* last_row, float* ms) {
+    return guard([&] {
+        std::lock_guard<std::mutex> g(e->mu);
+        RankCtx& R = session_rank(e);
+        const Shape& s = e->s;
+        KVP_CUDA(cudaEventRecord(R.ev_done, R.comp));
+        if (out_rows)
+            KVP_CUDA(cudaMemcpyAsync(out_rows, R.h.p, e->sess_rows * s.d * 4,
+                                     out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, R.comp));
+        if (last_row)
+            KVP_CUDA(cudaMemcpyAsync(last_row, R.h.as<float>() + (e->sess_rows - 1) * s.d, s.d * 4,
+                                     cudaMemcpyDeviceToHost, R.comp));
+        KVP_CUDA(cudaStreamSynchronize(R.comp));
+        float t = 0.f;
+        KVP_CUDA(cudaEventElapsedTime(&t, R.ev_begin, R.ev_done));
+        if (ms) *ms = t;
+        e->last_ttft = t;
+        e->in_session = false;
     });
 }
 

@@ -1,0 +1,282 @@
+"""Multi-process KV-Runahead: one process per GPU, one rank per process.
+
+The reference runs its ranks as threads exchanging typed messages through Channels
+(engine.hpp:223-296, channel.hpp).  Here each rank is a process (torchrun) that drives its
+own B200 layer executor through the per-rank C-ABI (kvp_rank_*), and the KV-cache handoff
+is point-to-point over a torch.distributed group -- NCCL over NVLink between GPUs, or gloo
+for CPU tests -- ordered on the executor's CUDA stream so layer l's transfer overlaps the
+sender's layer l+1 compute.
+
+Wire protocol (per link, per layer EXACTLY one message, so a collective transport can never
+deadlock): header int64[8] = {MAGIC, kind, layer, source, start, end, 0, 0} followed by the K
+and V rows.  The reference's fault injections (send_with_faults, engine.hpp:143-164) become
+edits of a per-link outbox: CorruptLayerTag bumps the header's layer, DropMessage leaves the
+slot to a CLOSED tombstone, DuplicateMessage re-queues the message so every later slot is
+shifted.  Receivers validate headers exactly like recv_checked (engine.hpp:166-179) after the
+run; the first error (lowest layer, then rank) is agreed over the group and raised on every
+rank, like Fabric::abort_all + rethrow_if_failed (channel.hpp:120-136).
+"""
+from __future__ import annotations
+
+import collections
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import kvprefill as kv
+
+HDR_LEN = 8
+MAGIC = 0x4B56524E
+KIND_HANDOFF, KIND_GATHER, KIND_CLOSED = 0, 1, 2
+_ERR_CODES = {kv.ProtocolError: 6, kv.CacheError: 3}
+_ERR_BY_CODE = {6: kv.ProtocolError, 3: kv.CacheError}
+
+
+# ------------------------------------------------------------------ transport
+class Transport:
+    """Blocking point-to-point tensor moves over a torch.distributed group.  With NCCL the
+    tensors stay on the GPU and the ops are ordered on the caller's current CUDA stream.  With
+    gloo, CUDA tensors are staged through host memory (shared-GPU / CPU test runs)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.backend = dist.get_backend(group)
+
+    def _staged(self, t) -> bool:
+        return self.backend == "gloo" and t.is_cuda
+
+    def exchange(self, sends, recvs):
+        """sends: [(tensor, dst)], recvs: [(tensor, src)] -- one batched group."""
+        import torch
+        dist = self.dist
+        staged_recv = []
+        ops = []
+        for t, dst in sends:
+            if self._staged(t):
+                torch.cuda.current_stream().synchronize()
+                t = t.cpu()
+            ops.append(dist.P2POp(dist.isend, t.contiguous(), dst, self.group))
+        for t, src in recvs:
+            if self._staged(t):
+                host = torch.empty(t.shape, dtype=t.dtype)
+                staged_recv.append((host, t))
+                t = host
+            ops.append(dist.P2POp(dist.irecv, t, src, self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        for host, dev in staged_recv:
+            dev.copy_(host, non_blocking=False)
+
+
+# ------------------------------------------------------------------ executors
+class GpuExecutor:
+    """One rank's B200 layer executor (kvp_rank_* C-ABI); K/V buffers are torch tensors so
+    the transport can address them."""
+
+    def __init__(self, weights: kv.WeightSet, device: int = 0):
+        import torch
+        self.torch = torch
+        self.w = weights
+        self.cfg = weights.config
+        self.device = torch.device("cuda", device)
+        self.dtype = torch.bfloat16 if self.cfg.precision == kv.Precision.bf16 else torch.float32
+        self._stream = None
+
+    def begin(self, rows, start: int, held: int):
+        torch = self.torch
+        import ctypes as C
+        L, kvd = self.cfg.n_layers, self.cfg.kv_dim()
+        self.kvbuf = torch.zeros((L, 2, held, kvd), dtype=self.dtype, device=self.device)
+        ptrs = (C.c_void_p * (2 * L))(*[self.kvbuf[l, i].data_ptr() for l in range(L) for i in range(2)])
+        if isinstance(rows, torch.Tensor):
+            rows_t = rows.to(self.device, torch.float32).contiguous()
+            self._rows = rows_t
+            ptr, on_dev = rows_t.data_ptr(), 1
+        else:
+            rows_np = np.ascontiguousarray(rows, dtype=np.float32)
+            self._rows = rows_np
+            ptr, on_dev = rows_np.ctypes.data, 0
+        self.n_rows = int(self._rows.shape[0])
+        kv._check(kv.lib().kvp_rank_begin(self.w.handle, C.c_void_p(ptr), self.n_rows, start, held, on_dev, ptrs),
+                  "rank_begin")
+        s = C.c_void_p()
+        kv._check(kv.lib().kvp_rank_stream(self.w.handle, C.byref(s)), "rank_stream")
+        self._stream = torch.cuda.ExternalStream(s.value, device=self.device)
+
+    def stream(self):
+        return self.torch.cuda.stream(self._stream)
+
+    def kv(self, layer: int):
+        return self.kvbuf[layer, 0], self.kvbuf[layer, 1]
+
+    def qkv(self, layer: int):
+        kv._check(kv.lib().kvp_rank_qkv(self.w.handle, layer), "rank_qkv")
+
+    def finish(self, layer: int, k_rows: int):
+        kv._check(kv.lib().kvp_rank_finish(self.w.handle, layer, k_rows), "rank_finish")
+
+    def end(self):
+        import ctypes as C
+        out = np.empty((self.n_rows, self.cfg.d_model), np.float32)
+        ms = C.c_float()
+        kv._check(kv.lib().kvp_rank_end(self.w.handle, C.c_void_p(out.ctypes.data), 0, None, C.byref(ms)), "rank_end")
+        return out, float(ms.value)
+
+    def header(self, values):
+        return self.torch.tensor(values, dtype=self.torch.int64, device=self.device)
+
+    def empty_header(self):
+        return self.torch.zeros(HDR_LEN, dtype=self.torch.int64, device=self.device)
+
+
+# ------------------------------------------------------------------ the rank driver
+@dataclass
+class RankResult:
+    hidden_rows: np.ndarray           # this rank's final hidden rows [c_i x d]
+    first_token_hidden: np.ndarray    # row C-1 (broadcast from the last rank), [1 x d]
+    metrics: kv.ExecutionMetrics      # global, identical on every rank
+    device_ms: float                  # this rank's device time
+    ttft_ms: float                    # max over ranks
+
+
+@dataclass
+class _Link:
+    outbox: collections.deque = field(default_factory=collections.deque)
+
+
+def _header(kind, layer, source, start, end):
+    return [MAGIC, kind, layer, source, start, end, 0, 0]
+
+
+def _apply_fault(fault: Optional[kv.FaultInjection], rank: int, msg: list, link: _Link, counter: list):
+    """send_with_faults (engine.hpp:143-164) as an outbox edit; returns nothing."""
+    pairs = msg[5] - msg[4]
+    K = kv.FaultInjection.Kind
+    if fault is not None and fault.kind != K.None_ and fault.rank == rank and fault.layer == msg[2]:
+        if fault.kind == K.DropMessage:
+            return
+        if fault.kind == K.CorruptLayerTag:
+            msg = list(msg)
+            msg[2] += 1
+        if fault.kind == K.DuplicateMessage:
+            link.outbox.append(list(msg))
+            counter[0] += pairs
+    link.outbox.append(list(msg))
+    counter[0] += pairs
+
+
+def _check_header(h, kind, layer, start_expected, end_expected):
+    """recv_checked (engine.hpp:166-179) + the KVR prefix check (engine.hpp:272-275)."""
+    h = [int(x) for x in h]
+    if h[0] != MAGIC or h[1] == KIND_CLOSED:
+        return kv.ProtocolError, "channel closed before message arrived"
+    if h[1] != kind:
+        return kv.ProtocolError, "unexpected message kind"
+    if h[2] != layer:
+        return kv.ProtocolError, (f"expected message for layer {layer}, got layer {h[2]} "
+                                  "(duplicate, dropped, or corrupt handoff)")
+    if not (0 <= h[4] < h[5]):
+        return kv.CacheError, "segment positions must satisfy 0 <= start < end"
+    if (h[4], h[5]) != (start_expected, end_expected):
+        return kv.CacheError, (f"handoff covers [{h[4]}, {h[5]}), expected [{start_expected}, {end_expected})")
+    return None
+
+
+def run_rank(strategy: kv.Strategy, rows, partition: kv.ContextPartition, executor, transport: Transport,
+             rank: int, world: int, n_layers: int, fault: Optional[kv.FaultInjection] = None,
+             group=None) -> RankResult:
+    """One rank of run(strategy, context, partition, weights, fault) (engine.hpp:186-318)."""
+    import torch.distributed as dist
+
+    partition.validate()
+    b = partition.boundaries
+    p = partition.process_count()
+    if p != world:
+        raise kv.InputError(f"partition has {p} ranks but the group has {world}")
+    if strategy == kv.Strategy.Serial and p != 1:
+        raise kv.InputError("serial strategy requires p == 1")
+    C_ = partition.context_length
+    start, stop = b[rank], b[rank + 1]
+    c = stop - start
+    held = stop if strategy == kv.Strategy.KVR else C_
+    executor.begin(rows, start, held)
+
+    dots = sent = recvd = waits = 0
+    barriers = 0
+    inbound = []  # (header tensor, kind, layer, expected start, expected end)
+    out_links = collections.defaultdict(_Link)
+    sent_ctr = [0]
+    for layer in range(n_layers):
+        executor.qkv(layer)
+        K, V = executor.kv(layer)
+        with executor.stream():
+            if strategy == kv.Strategy.KVR:
+                sends, recvs = [], []
+                if rank > 0:
+                    hin = executor.empty_header()
+                    recvs += [(hin, rank - 1), (K[:start], rank - 1), (V[:start], rank - 1)]
+                    inbound.append((hin, KIND_HANDOFF, layer, 0, start))
+                    waits += 1
+                    recvd += start
+                if rank + 1 < p:
+                    link = out_links[rank + 1]
+                    _apply_fault(fault, rank, _header(KIND_HANDOFF, layer, rank, 0, stop), link, sent_ctr)
+                    msg = link.outbox.popleft() if link.outbox else _header(KIND_CLOSED, layer, rank, 0, stop)
+                    sends += [(executor.header(msg), rank + 1), (K[:stop], rank + 1), (V[:stop], rank + 1)]
+                # the receive must land before the cumulative cache is forwarded
+                transport.exchange([], recvs)
+                transport.exchange(sends, [])
+                k_rows = stop
+            elif strategy == kv.Strategy.TSP:
+                sends, recvs = [], []
+                for peer in range(p):
+                    if peer == rank:
+                        continue
+                    link = out_links[peer]
+                    _apply_fault(fault, rank, _header(KIND_GATHER, layer, rank, start, stop), link, sent_ctr)
+                    msg = link.outbox.popleft() if link.outbox else _header(KIND_CLOSED, layer, rank, start, stop)
+                    sends += [(executor.header(msg), peer), (K[start:stop], peer), (V[start:stop], peer)]
+                    hin = executor.empty_header()
+                    lo, hi = b[peer], b[peer + 1]
+                    recvs += [(hin, peer), (K[lo:hi], peer), (V[lo:hi], peer)]
+                    inbound.append((hin, KIND_GATHER, layer, lo, hi))
+                    waits += 1
+                    recvd += hi - lo
+                transport.exchange(sends, recvs)  # the all-gather is the per-layer barrier
+                waits += 1
+                barriers += 1
+                k_rows = C_
+            else:
+                k_rows = C_
+        dots += c * k_rows
+        executor.finish(layer, k_rows)
+    hidden, ms = executor.end()
+    sent = sent_ctr[0]
+
+    # deferred recv_checked: first error by (layer, rank), agreed over the group
+    err = None
+    for hin, kind, layer, lo, hi in inbound:
+        res = _check_header(hin.cpu().tolist() if hasattr(hin, "cpu") else hin, kind, layer, lo, hi)
+        if res is not None:
+            err = (layer, rank, _ERR_CODES[res[0]], res[1])
+            break
+    everyone = [None] * world
+    dist.all_gather_object(everyone, {"err": err, "metrics": (dots, sent, recvd, waits), "ms": ms,
+                                      "last": hidden[-1:].tolist() if rank == world - 1 else None},
+                           group=group)
+    errs = [e["err"] for e in everyone if e["err"] is not None]
+    if errs:
+        first = min(errs, key=lambda t: (t[0], t[1]))
+        raise _ERR_BY_CODE[first[2]](f"rank {first[1]}: {first[3]}")
+    m = kv.ExecutionMetrics(n_layers=n_layers, barrier_count=barriers,
+                            dot_products=[e["metrics"][0] for e in everyone],
+                            kv_pairs_sent=[e["metrics"][1] for e in everyone],
+                            kv_pairs_received=[e["metrics"][2] for e in everyone],
+                            wait_events=[e["metrics"][3] for e in everyone])
+    ttft = max(e["ms"] for e in everyone)
+    first_token = np.asarray(everyone[-1]["last"], dtype=hidden.dtype)
+    return RankResult(hidden, first_token, m, ms, ttft)

@@ -114,6 +114,12 @@ _SIGS = {
     "kvp_engine_kernel_stats": (C.c_int, [_P, C.POINTER(_KStats), C.c_int32, C.POINTER(C.c_int32)]),
     "kvp_engine_profile_layer": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, C.POINTER(C.c_float),
                                            C.POINTER(C.c_float)]),
+    "kvp_rank_begin": (C.c_int, [_P, _P, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.POINTER(C.c_void_p)]),
+    "kvp_rank_stream": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
+    "kvp_rank_kv": (C.c_int, [_P, C.c_int64, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+    "kvp_rank_qkv": (C.c_int, [_P, C.c_int64]),
+    "kvp_rank_finish": (C.c_int, [_P, C.c_int64, C.c_int64]),
+    "kvp_rank_end": (C.c_int, [_P, _P, C.c_int32, _P, C.POINTER(C.c_float)]),
     "kvp_layer_qkv": (C.c_int, [_P, C.c_int64, _P, C.c_int64, _P, _P, _P]),
     "kvp_causal_attention": (C.c_int, [_P, _P, C.c_int64, _P, _P, C.c_int64, C.c_int64, _P]),
     "kvp_layer_finish": (C.c_int, [_P, C.c_int64, _P, C.c_int64, _P, _P, _P, C.c_int64, C.c_int64, _P]),

@@ -1,0 +1,75 @@
+"""Multi-process KV-Runahead on the GPU: two processes (ranks) sharing cuda:0 -- the only
+device this run has -- each driving its own B200 layer executor through the kvp_rank_* C-ABI,
+with the KV handoff moved by the distributed driver over gloo (host-staged; on a multi-GPU
+node the same code moves it with NCCL over NVLink).  The assembled result must equal the
+in-process engine bitwise (Serial == KVR across process boundaries)."""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, strategy, boundaries, outq):
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import oracle as O
+    from paper_2405_05329_b200 import kvprefill as kv
+    from paper_2405_05329_b200.distributed import GpuExecutor, Transport, run_rank
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    W = kv.init_weights(kv.ModelConfig(1024, 8, 2, 2, 5, "bf16", True), [0])
+    C_ = boundaries[-1]
+    ctx = O.random_context(C_, 1024, 11, np.float32)
+    strat = kv.Strategy.KVR if strategy == "kvr" else kv.Strategy.TSP
+    res = run_rank(strat, ctx[boundaries[rank]:boundaries[rank + 1]], kv.ContextPartition(C_, boundaries),
+                   GpuExecutor(W, 0), Transport(), rank, world, 2)
+    outq.put((rank, res.hidden_rows, res.metrics.__dict__))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("strategy,boundaries", [("kvr", [0, 300, 517]), ("tsp", [0, 259, 517])])
+def test_two_processes_match_in_process_engine(strategy, boundaries):
+    sys.path.insert(0, ROOT)
+    import oracle as O
+    from paper_2405_05329_b200 import kvprefill as kv
+    if kv.device_count() == 0:
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, strategy, boundaries, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in range(2):
+        rank, hidden, metrics = q.get(timeout=600)
+        got[rank] = (hidden, metrics)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    hidden = np.concatenate([got[0][0], got[1][0]])
+    W = kv.init_weights(kv.ModelConfig(1024, 8, 2, 2, 5, "bf16", True), [0])
+    C_ = boundaries[-1]
+    ref = kv.run(kv.Strategy.Serial, O.random_context(C_, 1024, 11, np.float32), kv.even_partition(C_, 1), W)
+    assert np.array_equal(hidden, ref.hidden_out)
+    strat = kv.Strategy.KVR if strategy == "kvr" else kv.Strategy.TSP
+    part = kv.ContextPartition(C_, boundaries)
+    assert got[0][1]["dot_products"] == [x * 2 for x in kv.dot_product_counts(strat, part)]
+    assert sum(got[0][1]["kv_pairs_sent"]) == 2 * kv.traffic_pairs(strat, part)
