@@ -155,6 +155,12 @@ kvp_status kvp_engine_kernel_stats(kvp_engine* e, kvp_kernel_stats* out, int32_t
 kvp_status kvp_engine_profile_layer(kvp_engine* e, int64_t rows, int64_t offset, int32_t reps, float* proj_ms,
                                     float* rest_ms);
 
+/* Kernel microbenchmark (tuning / ncu target): the tcgen05 GEMM D[M x N] = A[M x K] B[N x K]^T
+ * on devices[0] with random bf16 operands and epilogue kind epi (0 QKV-split, 1 residual,
+ * 2 ReLU, 3 store); median device ms over reps (CUDA events); bn_out = tile width used. */
+kvp_status kvp_bench_gemm(kvp_engine* e, int64_t M, int64_t N, int64_t K, int32_t epi, int32_t reps, float* ms,
+                          int32_t* bn_out);
+
 /* ------------------------------------------- one rank of a multi-process run */
 /* One process per GPU: the caller owns the transport (e.g. NCCL p2p via torch.distributed)
  * and drives one rank's per-layer schedule -- the worker loop of run<T>

@@ -245,10 +245,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(r[i]);
             }
             const int64_t key0 = static_cast<int64_t>(j) * BKV;
-            if (key0 + BKV - 1 > tile_first_abs) {  // tile crosses the causal diagonal
+            const bool diag = key0 + BKV - 1 > tile_first_abs;  // tile crosses the causal diagonal
+            if (diag) {
+                // keys [key0, key0 + nvis) are visible to this row; 32-bit compares against
+                // compile-time column indices, applied only on the diagonal tile
+                const int64_t v = abs_row - key0 + 1;
+                const int nvis = v < 0 ? 0 : (v > BKV ? BKV : static_cast<int>(v));
 #pragma unroll
-                for (int i = 0; i < BKV; ++i)
-                    if (key0 + i > abs_row) sv[i] = -INFINITY;
+                for (int i = 0; i < BKV; ++i) sv[i] = i < nvis ? sv[i] : -INFINITY;
             }
             float mx = -INFINITY;
 #pragma unroll
@@ -277,7 +281,6 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             const float nbv = (m_run == -INFINITY) ? 0.f : -m_run;
             const float2 sl2v = make_float2(a.sl2, a.sl2), nb2 = make_float2(nbv, nbv);
-            const bool diag = key0 + BKV - 1 > tile_first_abs;  // warp-uniform
             float2 lacc = make_float2(0.f, 0.f);
 #pragma unroll
             for (int c = 0; c < BKV / 32; ++c) {
@@ -294,9 +297,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                         pv.x = ex2_mufu(xv.x);
                         pv.y = ex2_mufu(xv.y);
                     }
-                    if (diag) {  // masked keys contribute exactly zero
-                        if (key0 + col > abs_row) pv.x = 0.f;
-                        if (key0 + col + 1 > abs_row) pv.y = 0.f;
+                    if (col >= POLY_FROM && diag) {  // the FMA-pipe exp2 clamps -inf: zero masked keys
+                        pv.x = sv[col] == -INFINITY ? 0.f : pv.x;
+                        pv.y = sv[col + 1] == -INFINITY ? 0.f : pv.y;
                     }
                     lacc = fadd2(lacc, pv);
                     pk[i] = ptx::pack_bf16(pv.x, pv.y);
@@ -371,15 +374,15 @@ void attn_bf16_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const At
     // KVP_ATTN_POLY = number of key columns (of 128) whose exp2 runs on the FMA pipe
     static const int poly = [] {
         const char* e = getenv("KVP_ATTN_POLY");
-        return e ? atoi(e) : 32;
+        return e ? atoi(e) : 0;
     }();
     if (sh.head_dim != 128 && sh.head_dim != 64) throw std::runtime_error("attn_tc: head_dim must be 64 or 128");
     const bool h128 = sh.head_dim == 128;
     switch (poly) {
-        case 0: h128 ? launch<128, 128>(Q, K, V, O, sh, s) : launch<64, 128>(Q, K, V, O, sh, s); break;
         case 48: h128 ? launch<128, 80>(Q, K, V, O, sh, s) : launch<64, 80>(Q, K, V, O, sh, s); break;
         case 64: h128 ? launch<128, 64>(Q, K, V, O, sh, s) : launch<64, 64>(Q, K, V, O, sh, s); break;
-        default: h128 ? launch<128, 96>(Q, K, V, O, sh, s) : launch<64, 96>(Q, K, V, O, sh, s); break;
+        case 32: h128 ? launch<128, 96>(Q, K, V, O, sh, s) : launch<64, 96>(Q, K, V, O, sh, s); break;
+        default: h128 ? launch<128, 128>(Q, K, V, O, sh, s) : launch<64, 128>(Q, K, V, O, sh, s); break;
     }
 }
 

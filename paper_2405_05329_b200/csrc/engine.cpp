@@ -1050,6 +1050,71 @@ kvp_status kvp_engine_profile_layer(kvp_engine* e, int64_t rows, int64_t offset,
     });
 }
 
+kvp_status kvp_bench_gemm(kvp_engine* e, int64_t M, int64_t N, int64_t K, int32_t epi, int32_t reps, float* ms,
+                          int32_t* bn_out) {
+    return guard([&] {
+        if (!e || !ms) throw Error(KVP_ERR_INPUT, "null argument");
+        if (M < 1 || N < 16 || K < 8 || reps < 1) throw Error(KVP_ERR_INPUT, "bad GEMM shape");
+        std::lock_guard<std::mutex> g(e->mu);
+        KVP_CUDA(cudaSetDevice(e->devices[0]));
+        DevBuf a, b, of, ob, rf;
+        a.ensure(M * K * 2, e->devices[0]);
+        b.ensure(N * K * 2, e->devices[0]);
+        of.ensure(M * N * 4, e->devices[0]);
+        ob.ensure(M * N * 2, e->devices[0]);
+        rf.ensure(M * N * 4, e->devices[0]);
+        DevBuf tmp;
+        tmp.ensure(std::max(M, N) * K * 4, e->devices[0]);
+        cudaStream_t st = nullptr;
+        launch_seeded_f32(tmp.as<float>(), M, K, 1.0, 11, st);
+        launch_cast_bf16(tmp.as<float>(), a.as<bf16>(), M * K, st);
+        launch_seeded_f32(tmp.as<float>(), N, K, 0.02, 12, st);
+        launch_cast_bf16(tmp.as<float>(), b.as<bf16>(), N * K, st);
+        launch_seeded_f32(rf.as<float>(), M, N, 1.0, 13, st);
+        GemmEpilogue ep;
+        ep.kind = epi;
+        ep.out0 = ob.as<bf16>();
+        ep.ld0 = N;
+        ep.n0 = N;
+        if (epi == EPI_QKV) {  // split like a fused Wqkv: q = N - 2*(N/6) ... three column blocks
+            const int64_t kvw = ((N / 6) / 32) * 32;
+            ep.n0 = N - 2 * kvw;
+            ep.ld0 = ep.n0;
+            ep.out1 = ob.as<bf16>() + M * ep.n0;
+            ep.ld1 = kvw;
+            ep.n1 = kvw;
+            ep.out2 = ep.out1 + M * kvw;
+            ep.ld2 = kvw;
+        }
+        ep.outf = of.as<float>();
+        ep.ldf = N;
+        ep.resid = rf.as<float>();
+        ep.ldr = N;
+        if (epi == EPI_RESID) {
+            ep.outb = ob.as<bf16>();
+            ep.ldb = N;
+        }
+        cudaEvent_t e0, e1;
+        KVP_CUDA(cudaEventCreate(&e0));
+        KVP_CUDA(cudaEventCreate(&e1));
+        std::vector<float> t;
+        for (int i = 0; i < reps + 1; ++i) {
+            KVP_CUDA(cudaEventRecord(e0, st));
+            gemm_bf16_tc(a.as<bf16>(), M, K, b.as<bf16>(), N, ep, st);
+            KVP_CUDA(cudaEventRecord(e1, st));
+            KVP_CUDA(cudaEventSynchronize(e1));
+            float x = 0;
+            KVP_CUDA(cudaEventElapsedTime(&x, e0, e1));
+            if (i) t.push_back(x);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        std::sort(t.begin(), t.end());
+        *ms = t[t.size() / 2];
+        if (bn_out) *bn_out = gemm_bf16_tc_bn(M, N);
+    });
+}
+
 kvp_status kvp_rank_begin(kvp_engine* e, const float* rows, int64_t n_rows, int64_t start, int64_t held,
                           int32_t rows_on_device, void* const* kv_bufs) {
     return guard([&] {

@@ -363,11 +363,7 @@ void dispatch(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
 
 }  // namespace
 
-void gemm_bf16_tc(const bf16* A, int64_t M, int64_t K, const bf16* B, int64_t N, const GemmEpilogue& ep,
-                  cudaStream_t s) {
-    if (M <= 0 || N <= 0) return;
-    if (K % 8 != 0 || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15))
-        throw std::runtime_error("gemm_bf16_tc: K must be a multiple of 8 and operands 16-byte aligned");
+int gemm_bf16_tc_bn(int64_t M, int64_t N) {
     // Tile width: BN=256 feeds the tensor core with the least smem traffic per FLOP; BN=128
     // halves the tile so the persistent grid quantises better (e.g. 4096x4096 outputs are 512
     // tiles = 3.46 waves of 148 SMs at BN=256 but 6.92 waves at BN=128).  Pick the width with
@@ -387,7 +383,16 @@ void gemm_bf16_tc(const bf16* A, int64_t M, int64_t K, const bf16* B, int64_t N,
     if (N < 256) wide = false;
     if (forced == 128) wide = false;
     if (forced == 256 && N >= 256) wide = true;
-    const int BN = wide ? 256 : 128;
+    return wide ? 256 : 128;
+}
+
+void gemm_bf16_tc(const bf16* A, int64_t M, int64_t K, const bf16* B, int64_t N, const GemmEpilogue& ep,
+                  cudaStream_t s) {
+    if (M <= 0 || N <= 0) return;
+    if (K % 8 != 0 || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15))
+        throw std::runtime_error("gemm_bf16_tc: K must be a multiple of 8 and operands 16-byte aligned");
+    const int BN = gemm_bf16_tc_bn(M, N);
+    const bool wide = BN == 256;
     CUtensorMap ta, tb;
     if (!make_tmap_bf16(&ta, A, K, M, K, BK, BM) || !make_tmap_bf16(&tb, B, K, N, K, BK, BN)) {
         char msg[160];

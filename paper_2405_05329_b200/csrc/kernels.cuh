@@ -74,6 +74,8 @@ struct GemmEpilogue {
 inline int ssq_parts_for(int64_t cols) { return static_cast<int>((cols + 127) / 128); }
 void gemm_bf16_tc(const bf16* A, int64_t M, int64_t K, const bf16* B, int64_t N, const GemmEpilogue& ep,
                   cudaStream_t s);
+// tile width the dispatcher picks for this shape (128 or 256)
+int gemm_bf16_tc_bn(int64_t M, int64_t N);
 
 // ---------------------------------------------------------------- gemm_simt.cu
 // fp32 parity GEMM: C = A[M x K] . B[K x N] (reference layout), sequential k order with

@@ -114,6 +114,8 @@ _SIGS = {
     "kvp_engine_kernel_stats": (C.c_int, [_P, C.POINTER(_KStats), C.c_int32, C.POINTER(C.c_int32)]),
     "kvp_engine_profile_layer": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, C.POINTER(C.c_float),
                                            C.POINTER(C.c_float)]),
+    "kvp_bench_gemm": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_float),
+                                 C.POINTER(C.c_int32)]),
     "kvp_rank_begin": (C.c_int, [_P, _P, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.POINTER(C.c_void_p)]),
     "kvp_rank_stream": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
     "kvp_rank_kv": (C.c_int, [_P, C.c_int64, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
@@ -401,6 +403,12 @@ class WeightSet:
         a, b = C.c_float(), C.c_float()
         _check(lib().kvp_engine_profile_layer(self._h, rows, offset, reps, C.byref(a), C.byref(b)), "profile_layer")
         return float(a.value), float(b.value)
+
+    def bench_gemm(self, M: int, N: int, K: int, epi: int = 3, reps: int = 10):
+        """(median ms, TFLOP/s, tile width) of one tcgen05 GEMM shape in isolation."""
+        ms, bn = C.c_float(), C.c_int32()
+        _check(lib().kvp_bench_gemm(self._h, M, N, K, epi, reps, C.byref(ms), C.byref(bn)), "bench_gemm")
+        return float(ms.value), 2.0 * M * N * K / (ms.value * 1e-3) / 1e12, int(bn.value)
 
     def last_launch_count(self) -> int:
         v = C.c_int64()
