@@ -71,7 +71,8 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int STAGES = 4;
-constexpr int THREADS = 192;
+constexpr int THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (2 per TMEM lane quarter)
+constexpr int EPI_WARPS = 8;
 
 template <int BN>
 struct Cfg {
@@ -138,11 +139,14 @@ __device__ __forceinline__ float store_chunk(const EpiArgs& ep, int64_t row, int
                 }
             }
         } else {
-            for (int j = 0; j < 32 && col0 + j < N; ++j) {
-                const float v = rs[j] + __uint_as_float(r[j]);
-                o[j] = v;
-                ss += v * v;
-                if (ob) ob[j] = __float2bfloat16_rn(v);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                if (col0 + j < N) {
+                    const float v = rs[j] + __uint_as_float(r[j]);
+                    o[j] = v;
+                    ss += v * v;
+                    if (ob) ob[j] = __float2bfloat16_rn(v);
+                }
             }
         }
     } else {
@@ -152,7 +156,9 @@ __device__ __forceinline__ float store_chunk(const EpiArgs& ep, int64_t row, int
             // take the per-element path
             const int64_t e0 = ep.n0, e1 = ep.n0 + ep.n1;
             if ((col0 < e0 && col0 + 32 > e0) || (col0 < e1 && col0 + 32 > e1)) {
-                for (int j = 0; j < 32 && col0 + j < N; ++j) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    if (col0 + j >= N) continue;
                     const int64_t c = col0 + j;
                     bf16* dst = c < e0 ? ep.out0 + row * ep.ld0 + c
                                        : (c < e1 ? ep.out1 + row * ep.ld1 + (c - e0) : ep.out2 + row * ep.ld2 + (c - e1));
@@ -187,7 +193,9 @@ __device__ __forceinline__ float store_chunk(const EpiArgs& ep, int64_t row, int
                 *reinterpret_cast<uint4*>(o + j) = pk;
             }
         } else {
-            for (int j = 0; j < 32 && col0 + j < N; ++j) o[j] = __float2bfloat16_rn(v[j]);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (col0 + j < N) o[j] = __float2bfloat16_rn(v[j]);
         }
     }
     return ss;
@@ -222,7 +230,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(&tfull[b], 1);
-            ptx::mbar_init(&tempty[b], 4);
+            ptx::mbar_init(&tempty[b], EPI_WARPS);
         }
         ptx::fence_barrier_init();
     }
@@ -282,8 +290,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     } else {
-        // Epilogue warps 2..5: warp w may touch TMEM lanes [32*(w%4), 32*(w%4)+32).
+        // Epilogue warps 2..9: warp w may touch TMEM lanes [32*(w%4), 32*(w%4)+32); the two
+        // warps of a lane quarter split the tile's columns (more loads in flight per row).
         const uint32_t quarter = warp & 3;
+        const int half = (warp - 2) >> 2;
+        constexpr int CHUNKS = BN / 32, MY = CHUNKS / 2;
         int t = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
             const int m_blk = tile % num_m, n_blk = tile / num_m;
@@ -303,7 +314,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             float ssacc = 0.f;
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int cc = 0; cc < MY; ++cc) {
+                const int c = half * MY + cc;
                 const int64_t col0 = static_cast<int64_t>(n_blk) * BN + c * 32;
                 if (col0 >= N) break;  // warp-uniform
                 uint32_t r[32];
@@ -311,9 +323,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                 ptx::tmem_ld_wait();
                 if (row < M) ssacc += store_chunk<KIND>(ep, row, col0, N, r, row_scale);
                 if constexpr (KIND == EPI_RESID) {
-                    // one partial per 128-column group, independent of BN (deterministic)
-                    if (ep.ssq_out != nullptr && row < M && (((c + 1) & 3) == 0 || col0 + 32 >= N)) {
-                        ep.ssq_out[row * ep.ssq_parts + (col0 >> 7)] = ssacc;
+                    // one partial per 64-column group, independent of BN and of the warp split
+                    if (ep.ssq_out != nullptr && row < M && (((c + 1) & 1) == 0 || col0 + 32 >= N)) {
+                        ep.ssq_out[row * ep.ssq_parts + (col0 >> 6)] = ssacc;
                         ssacc = 0.f;
                     }
                 }

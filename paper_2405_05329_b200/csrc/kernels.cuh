@@ -34,7 +34,7 @@ void launch_norm_cast_bf16(const float* x, bf16* y, int64_t rows, int64_t cols, 
 // f32 rms_norm_rows with the reference's sequential accumulation order (bit-exact).
 void launch_norm_f32(const float* x, float* y, int64_t rows, int64_t cols, cudaStream_t s);
 void launch_cast_bf16(const float* x, bf16* y, int64_t n, cudaStream_t s);
-// y = bf16(x) and ssq[r, g] = sum of x^2 over columns [128g, 128g+128) of row r (the layer-0
+// y = bf16(x) and ssq[r, g] = sum of x^2 over columns [64g, 64g+64) of row r (the layer-0
 // input of the fused-norm pipeline; later layers get both from the GEMM epilogues).
 void launch_prep_bf16_ssq(const float* x, bf16* y, float* ssq, int64_t rows, int64_t cols, cudaStream_t s);
 void launch_cast_f32(const bf16* x, float* y, int64_t n, cudaStream_t s);
@@ -60,8 +60,8 @@ struct GemmEpilogue {
     const float* resid = nullptr;
     int64_t ldr = 0;
     // Fused RMSNorm (model.hpp:29-45).  Producer side (EPI_RESID): also write bf16(out) to
-    // outb and per-row partial sums of squares over each 128-column group to ssq_out
-    // [rows x ceil(N/128)].  Consumer side (EPI_QKV / EPI_RELU / EPI_STORE): scale row r of
+    // outb and per-row partial sums of squares over each 64-column group to ssq_out
+    // [rows x ceil(N/64)].  Consumer side (EPI_QKV / EPI_RELU / EPI_STORE): scale row r of
     // the accumulator by (sum(ssq_in[r,:]) / norm_cols + 1e-6)^-1/2 before the epilogue op
     // (norm(x).W == diag(1/rms).(x.W); ReLU commutes with the positive scale).
     bf16* outb = nullptr;
@@ -71,7 +71,7 @@ struct GemmEpilogue {
     int ssq_parts = 0;
     int64_t norm_cols = 0;
 };
-inline int ssq_parts_for(int64_t cols) { return static_cast<int>((cols + 127) / 128); }
+inline int ssq_parts_for(int64_t cols) { return static_cast<int>((cols + 63) / 64); }
 void gemm_bf16_tc(const bf16* A, int64_t M, int64_t K, const bf16* B, int64_t N, const GemmEpilogue& ep,
                   cudaStream_t s);
 // tile width the dispatcher picks for this shape (128 or 256)

@@ -57,28 +57,24 @@ __global__ void norm_f32_kernel(const float* __restrict__ x, float* __restrict__
     for (int64_t c = 0; c < cols; ++c) y[r * cols + c] = __fmul_rn(xr[c], inv);
 }
 
-// One warp per row; each 128-column group is one float4 per lane, reduced in a fixed
+// One warp per row; each 64-column group is one float2 per lane, reduced in a fixed
 // shuffle order (deterministic).
 __global__ void prep_bf16_ssq_kernel(const float* __restrict__ x, bf16* __restrict__ y, float* __restrict__ ssq,
                                      int64_t rows, int64_t cols) {
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
     const int lane = threadIdx.x & 31;
-    const int parts = static_cast<int>((cols + 127) / 128);
+    const int parts = static_cast<int>((cols + 63) / 64);
     for (int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; r < rows; r += warps) {
         const float* xr = x + r * cols;
         bf16* yr = y + r * cols;
         for (int g = 0; g < parts; ++g) {
-            const int64_t c = static_cast<int64_t>(g) * 128 + lane * 4;
+            const int64_t c = static_cast<int64_t>(g) * 64 + lane * 2;
             float ss = 0.f;
             if (c < cols) {
-                const float4 v = *reinterpret_cast<const float4*>(xr + c);
-                ss = v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+                const float2 v = *reinterpret_cast<const float2*>(xr + c);
+                ss = v.x * v.x + v.y * v.y;
                 __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y);
-                __nv_bfloat162 b = __floats2bfloat162_rn(v.z, v.w);
-                uint2 pk;
-                pk.x = *reinterpret_cast<uint32_t*>(&a);
-                pk.y = *reinterpret_cast<uint32_t*>(&b);
-                *reinterpret_cast<uint2*>(yr + c) = pk;
+                *reinterpret_cast<__nv_bfloat162*>(yr + c) = a;
             }
             for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
             if (lane == 0) ssq[r * parts + g] = ss;
