@@ -231,6 +231,22 @@ kvp_status kvp_search_partition(int64_t C, int64_t p, int64_t n_layers, const kv
 /* practical_bound (simnet.hpp:297-316). */
 kvp_status kvp_practical_bound(int64_t C, int64_t p, int64_t n_layers, const kvp_cost_model* cost,
                                int64_t* boundaries_out, double* ttft_out);
+/* simulate_ttft with a NoiseSidecar{seed, slowdown_factor} (simnet.hpp:65-78,136-141). */
+kvp_status kvp_simulate_ttft_noisy(int32_t strategy, int64_t C, const int64_t* boundaries, int64_t p,
+                                   int64_t n_layers, const kvp_cost_model* cost, const kvp_network_model* net,
+                                   uint64_t noise_seed, double slowdown_factor, double* ttft_out);
+/* noise_study (simnet.hpp:332-353): per_trial (nullable) gets `trials` degradations. */
+kvp_status kvp_noise_study(int32_t strategy, int64_t C, const int64_t* boundaries, int64_t p, int64_t n_layers,
+                           const kvp_cost_model* cost, const kvp_network_model* net, double slowdown_factor,
+                           int64_t trials, uint64_t seed, double* quiet_ttft, double* mean_degradation,
+                           double* max_degradation, double* per_trial);
+/* KVR-P: PartitionLookupTable (lookup_table.hpp:22-39) given as n entries of
+ * (context_lengths[i], ratios[i*p .. i*p+p)); interpolate_partition (lookup_table.hpp:44-64)
+ * and partition_from_table (lookup_table.hpp:68-70). */
+kvp_status kvp_interpolate_partition(const int64_t* context_lengths, const double* ratios, int64_t n, int64_t p,
+                                     int64_t C, double* ratios_out);
+kvp_status kvp_partition_from_table(const int64_t* context_lengths, const double* ratios, int64_t n, int64_t p,
+                                    int64_t C, int64_t* boundaries_out);
 /* Least-squares fit of CostModel{proj_coeff, alpha, softmax_coeff=0, fixed_overhead} from
  * measured per-layer times (new: the reference only fits alpha, simnet.hpp:356).
  * Samples i: local_rows[i], held_rows[i], proj_s[i] (norm+QKV seconds) and rest_s[i]

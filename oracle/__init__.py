@@ -497,6 +497,32 @@ class Reference:
         _check(fn(C_, p, n_layers, C.byref(cc), _ptr(out), C.byref(t)), "ref practical_bound")
         return out.tolist(), t.value
 
+    def noise_study(self, strategy, boundaries, n_layers, factor, trials, seed, cost=None, net=None):
+        cost = cost or CostModel()
+        net = net or NetworkModel()
+        b, _ = _i64(boundaries)
+        q, mean, mx = C.c_double(), C.c_double(), C.c_double()
+        per = np.zeros(max(trials, 1), np.float64)
+        fn = self.lib.kvref_noise_study
+        fn.argtypes = [C.c_int, C.c_int64, C.c_void_p, C.c_int64, C.c_int64, C.POINTER(_Cost), C.POINTER(_Net),
+                       C.c_double, C.c_int64, C.c_uint64, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                       C.POINTER(C.c_double), C.c_void_p]
+        cc, nc = cost.c(), net.c()
+        _check(fn(strategy, int(b[-1]), _ptr(b), len(b) - 1, n_layers, C.byref(cc), C.byref(nc), factor, trials,
+                  seed, C.byref(q), C.byref(mean), C.byref(mx), _ptr(per)), "ref noise_study")
+        return q.value, mean.value, mx.value, per[:trials].tolist()
+
+    def table(self, entries: dict, p: int, C_: int):
+        keys = list(entries)
+        Cs = np.ascontiguousarray(keys, np.int64)
+        R = np.ascontiguousarray([entries[k] for k in keys], np.float64)
+        rout = np.zeros(p, np.float64)
+        bout = np.zeros(p + 1, np.int64)
+        fn = self.lib.kvref_table
+        fn.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
+        _check(fn(_ptr(Cs), _ptr(R), len(keys), p, C_, _ptr(rout), _ptr(bout)), "ref table")
+        return rout.tolist(), bout.tolist()
+
     def causal_attention(self, m: Model, Q, K, V, offset):
         dtype = np.float64 if m.precision == "f64" else np.float32
         Q, K, V = (np.ascontiguousarray(x, dtype) for x in (Q, K, V))

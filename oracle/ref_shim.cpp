@@ -280,6 +280,36 @@ int kvref_practical_bound(int64_t C, int64_t p, int64_t n_layers, const RefCost*
     })
 }
 
+// noise_study (simnet.hpp:332-353)
+int kvref_noise_study(int strategy, int64_t C, const int64_t* b, int64_t p, int64_t n_layers, const RefCost* cost,
+                      const RefNet* net, double factor, int64_t trials, uint64_t seed, double* quiet, double* mean,
+                      double* mx, double* per_trial) {
+    GUARD({
+        ModelConfig m;
+        m.n_layers = n_layers;
+        const auto st = noise_study(static_cast<Strategy>(strategy), to_part(C, b, p), m, to_cost(cost), to_net(net),
+                                    factor, trials, seed);
+        *quiet = st.quiet_ttft;
+        *mean = st.mean_degradation;
+        *mx = st.max_degradation;
+        for (size_t i = 0; i < st.per_trial.size(); ++i) per_trial[i] = st.per_trial[i];
+    })
+}
+
+// interpolate_partition / partition_from_table (lookup_table.hpp:44-70)
+int kvref_table(const int64_t* Cs, const double* ratios, int64_t n, int64_t p, int64_t C, double* ratios_out,
+                int64_t* boundaries_out) {
+    GUARD({
+        PartitionLookupTable t;
+        t.process_count = p;
+        for (int64_t i = 0; i < n; ++i) t.insert(Cs[i], std::vector<double>(ratios + i * p, ratios + (i + 1) * p));
+        const auto r = interpolate_partition(t, C);
+        std::memcpy(ratios_out, r.data(), r.size() * sizeof(double));
+        const auto part = partition_from_table(t, C);
+        std::memcpy(boundaries_out, part.boundaries.data(), part.boundaries.size() * sizeof(int64_t));
+    })
+}
+
 int kvref_ttft_star(int64_t C, int64_t p, double alpha, double* out) { GUARD({ *out = ttft_star(C, p, alpha); }) }
 
 double kvref_table_build_cost(double T, int64_t N, int64_t C) { return table_build_cost(T, N, C); }

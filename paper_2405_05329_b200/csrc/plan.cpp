@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <map>
 #include <numeric>
 #include <unordered_map>
 #include <vector>
@@ -95,8 +96,36 @@ static void check_net(const kvp_network_model& n) {
 
 static double wire_seconds(double pairs, double bw, double lat) { return pairs <= 0 ? 0.0 : lat + pairs / bw; }
 
+// NoiseSidecar (simnet.hpp:65-78): per layer one adjacent link, drawn from (seed, layer) only,
+// runs at bandwidth / factor.
+struct Noise {
+    bool on = false;
+    uint64_t seed = 1;
+    double factor = 1.0;
+};
+
+static uint64_t sm_next(uint64_t& s) {
+    uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+static uint64_t mix(uint64_t base, uint64_t a, uint64_t b) {
+    uint64_t g = base;
+    uint64_t h = sm_next(g) ^ (a * 0xd1342543de82ef95ULL);
+    return sm_next(h) ^ (b * 0xaf251af3b0f025b5ULL);
+}
+
+static double link_bw(const kvp_network_model& net, const Noise& nz, int64_t layer, int64_t link, int64_t links) {
+    if (nz.on && nz.factor > 1.0 && links >= 1) {
+        uint64_t st = mix(nz.seed, 0x6e6fu, static_cast<uint64_t>(layer));
+        if (static_cast<int64_t>(sm_next(st) % static_cast<uint64_t>(links)) == link) return net.bandwidth / nz.factor;
+    }
+    return net.bandwidth;
+}
+
 double simulate(int32_t strategy, int64_t C, const int64_t* b, int64_t p, int64_t L, const kvp_cost_model& cost,
-                const kvp_network_model& net) {
+                const kvp_network_model& net, const Noise& nz = Noise{}) {
     check_partition(C, b, p);
     check_cost(cost);
     check_net(net);
@@ -112,7 +141,7 @@ double simulate(int32_t strategy, int64_t C, const int64_t* b, int64_t p, int64_
             double worst = 0.0;
             for (int64_t k = 0; k + 1 < p; ++k) {
                 const double share = static_cast<double>(std::max(b[k + 1], C - b[k + 1]));
-                worst = std::max(worst, net.latency + share / net.bandwidth);
+                worst = std::max(worst, net.latency + share / link_bw(net, nz, layer, k, p - 1));
             }
             const double released = gather + rounds * worst;
             for (int64_t i = 0; i < p; ++i) {
@@ -128,7 +157,7 @@ double simulate(int32_t strategy, int64_t C, const int64_t* b, int64_t p, int64_
                 const double ready = i > 0 ? std::max(pe, up_start + up_wire) : pe;
                 double sent = -std::numeric_limits<double>::infinity();
                 if (i + 1 < p) {
-                    const double w = wire_seconds(static_cast<double>(held), net.bandwidth, net.latency);
+                    const double w = wire_seconds(static_cast<double>(held), link_bw(net, nz, layer, i, p - 1), net.latency);
                     sent = ready + w;
                     up_start = ready;
                     up_wire = w;
@@ -462,6 +491,92 @@ kvp_status kvp_practical_bound(int64_t C, int64_t p, int64_t L, const kvp_cost_m
         const Bounds b = grid_search(C, p, cfg, sim_eval, &u, &r);
         std::memcpy(out, b.data(), b.size() * sizeof(int64_t));
         *ttft = r.ttft;
+    });
+}
+
+kvp_status kvp_simulate_ttft_noisy(int32_t strategy, int64_t C, const int64_t* b, int64_t p, int64_t L,
+                                   const kvp_cost_model* cost, const kvp_network_model* net, uint64_t noise_seed,
+                                   double factor, double* out) {
+    return guard([&] {
+        Noise nz;
+        nz.on = true;
+        nz.seed = noise_seed;
+        nz.factor = factor;
+        *out = simulate(strategy, C, b, p, L, *cost, *net, nz);
+    });
+}
+
+kvp_status kvp_noise_study(int32_t strategy, int64_t C, const int64_t* b, int64_t p, int64_t L,
+                           const kvp_cost_model* cost, const kvp_network_model* net, double factor, int64_t trials,
+                           uint64_t seed, double* quiet, double* mean, double* mx, double* per_trial) {
+    return guard([&] {
+        if (trials < 1) throw Error(KVP_ERR_INPUT, "noise_study requires trials >= 1");
+        if (!(factor >= 1.0)) throw Error(KVP_ERR_CONFIG, "slowdown_factor must be >= 1");
+        const double q = simulate(strategy, C, b, p, L, *cost, *net);
+        double sum = 0.0, worst = 0.0;
+        for (int64_t t = 0; t < trials; ++t) {
+            Noise nz;
+            nz.on = true;
+            nz.seed = mix(seed, 0x7472u, static_cast<uint64_t>(t));
+            nz.factor = factor;
+            const double d = (simulate(strategy, C, b, p, L, *cost, *net, nz) - q) / q;
+            if (per_trial) per_trial[t] = d;
+            sum += d;
+            worst = std::max(worst, d);
+        }
+        *quiet = q;
+        *mean = sum / static_cast<double>(trials);
+        *mx = worst;
+    });
+}
+
+// PartitionLookupTable::insert validation (lookup_table.hpp:26-38) + interpolate_partition.
+static std::vector<double> interpolate(const int64_t* Cs, const double* ratios, int64_t n, int64_t p, int64_t C) {
+    if (p < 1) throw Error(KVP_ERR_LOOKUP, "table process count not set");
+    std::map<int64_t, std::vector<double>> entries;
+    for (int64_t i = 0; i < n; ++i) {
+        std::vector<double> r(ratios + i * p, ratios + (i + 1) * p);
+        double sum = 0;
+        for (double x : r) {
+            if (x < 0) throw Error(KVP_ERR_LOOKUP, "table ratios must be non-negative");
+            sum += x;
+        }
+        if (std::abs(sum - 1.0) > 1e-9) throw Error(KVP_ERR_LOOKUP, "table ratios must sum to 1");
+        if (Cs[i] < 1) throw Error(KVP_ERR_LOOKUP, "context length must be positive");
+        entries[Cs[i]] = std::move(r);
+    }
+    if (entries.empty()) throw Error(KVP_ERR_LOOKUP, "lookup table is empty");
+    const auto hit = entries.find(C);
+    if (hit != entries.end()) return hit->second;
+    const auto hi = entries.upper_bound(C);
+    if (hi == entries.begin()) return hi->second;          // below range: clamp
+    if (hi == entries.end()) return std::prev(hi)->second;  // above range: clamp
+    const auto lo = std::prev(hi);
+    const double t = static_cast<double>(C - lo->first) / static_cast<double>(hi->first - lo->first);
+    std::vector<double> out(lo->second.size());
+    double sum = 0;
+    for (size_t i = 0; i < out.size(); ++i) {
+        out[i] = (1.0 - t) * lo->second[i] + t * hi->second[i];
+        sum += out[i];
+    }
+    for (double& r : out) r /= sum;
+    return out;
+}
+
+kvp_status kvp_interpolate_partition(const int64_t* Cs, const double* ratios, int64_t n, int64_t p, int64_t C,
+                                     double* out) {
+    return guard([&] {
+        const auto r = interpolate(Cs, ratios, n, p, C);
+        std::memcpy(out, r.data(), r.size() * sizeof(double));
+    });
+}
+
+kvp_status kvp_partition_from_table(const int64_t* Cs, const double* ratios, int64_t n, int64_t p, int64_t C,
+                                    int64_t* out) {
+    return guard([&] {
+        const auto r = interpolate(Cs, ratios, n, p, C);
+        const Bounds b = ratio_split(C, r.data(), static_cast<int64_t>(r.size()));
+        std::memcpy(out, b.data(), b.size() * sizeof(int64_t));
     });
 }
 

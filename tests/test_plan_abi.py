@@ -166,3 +166,100 @@ def test_fit_cost_model_recovers_generator():
         assert abs(getattr(fit, k) / getattr(true, k) - 1) < 1e-6, k
     with pytest.raises(kv.CalibrationError):
         kv.fit_cost_model([], [], [], [])
+
+
+# ---------------------------------------------------------------- SURVEY 8f next rows
+def test_noise_study_semantics():  # test_simnet.cpp:128-184
+    part = kv.even_partition(1024, 4)
+    m = kv.ModelConfig(n_layers=2)
+    quiet = kv.noise_study(kv.Strategy.TSP, part, m, kv.CostModel(), kv.NetworkModel(), 1.0, 8, 42)
+    assert quiet.mean_degradation == 0.0 and quiet.max_degradation == 0.0 and all(d == 0.0 for d in quiet.per_trial)
+    a = kv.noise_study(kv.Strategy.TSP, part, m, kv.CostModel(), kv.NetworkModel(), 16.0, 12, 9)
+    b = kv.noise_study(kv.Strategy.TSP, part, m, kv.CostModel(), kv.NetworkModel(), 16.0, 12, 9)
+    assert a.per_trial == b.per_trial
+    harsh = kv.noise_study(kv.Strategy.TSP, part, m, kv.CostModel(), kv.NetworkModel(), 256.0, 12, 9)
+    assert harsh.mean_degradation >= a.mean_degradation and harsh.max_degradation >= a.max_degradation
+    tsp = kv.noise_study(kv.Strategy.TSP, part, m, kv.CostModel(), kv.NetworkModel(), 256.0, 12, 7)
+    kvr = kv.noise_study(kv.Strategy.KVR, part, m, kv.CostModel(), kv.NetworkModel(), 256.0, 12, 7)
+    assert tsp.mean_degradation > kvr.mean_degradation
+    with pytest.raises(kv.InputError):
+        kv.noise_study(kv.Strategy.TSP, part, m, kv.CostModel(), kv.NetworkModel(), 16.0, 0, 9)
+    with pytest.raises(kv.ConfigError):
+        kv.noise_study(kv.Strategy.TSP, part, m, kv.CostModel(), kv.NetworkModel(), 0.5, 4, 9)
+
+
+def test_acceptance_criterion7_noise():  # acceptance.cpp:290-313
+    even = kv.even_partition(2048, 4)
+    m = kv.ModelConfig(n_layers=2)
+    factor = 4.0
+    while factor <= 1048576.0:
+        tsp = kv.noise_study(kv.Strategy.TSP, even, m, kv.CostModel(), kv.NetworkModel(), factor, 20, 2026)
+        if tsp.mean_degradation >= 0.08:
+            kvr = kv.noise_study(kv.Strategy.KVR, even, m, kv.CostModel(), kv.NetworkModel(), factor, 20, 2026)
+            assert kvr.mean_degradation < tsp.mean_degradation
+            return
+        factor *= 2.0
+    raise AssertionError("gather never reached 8% mean degradation")
+
+
+def test_lookup_table_interpolation_and_io(tmp_path):  # test_table_io.cpp:38-112
+    t = kv.PartitionLookupTable(2)
+    t.insert(1000, [0.6, 0.4])
+    t.insert(3000, [0.7, 0.3])
+    assert kv.interpolate_partition(t, 1000) == [0.6, 0.4]
+    mid = kv.interpolate_partition(t, 2000)
+    assert abs(mid[0] - 0.65) < 1e-12 and abs(sum(mid) - 1) < 1e-15
+    assert kv.interpolate_partition(t, 10) == [0.6, 0.4]      # clamp below
+    assert kv.interpolate_partition(t, 9000) == [0.7, 0.3]    # clamp above
+    assert kv.partition_from_table(t, 2000).sizes() == [1300, 700]
+    with pytest.raises(kv.LookupError_):
+        kv.interpolate_partition(kv.PartitionLookupTable(2), 10)
+    with pytest.raises(kv.LookupError_):
+        t.insert(5, [0.5, 0.4])
+    path = str(tmp_path / "table.json")
+    t.save(path)
+    again = kv.PartitionLookupTable.load(path)
+    assert again.entries == t.entries and again.process_count == 2
+    (tmp_path / "bad.json").write_text("{not json")
+    with pytest.raises(kv.LookupError_):
+        kv.PartitionLookupTable.load(str(tmp_path / "bad.json"))
+    with pytest.raises(kv.IoError):
+        kv.PartitionLookupTable.load(str(tmp_path / "missing.json"))
+
+
+def test_acceptance_criterion6_table_vs_fresh_search():  # acceptance.cpp:251-286
+    m = kv.ModelConfig(n_layers=2)
+    t = kv.PartitionLookupTable(4)
+    for C_ in (512, 2560, 4608, 6656):
+        found = kv.search_partition(C_, 4, m, kv.CostModel(), kv.NetworkModel())
+        t.insert(C_, [c / C_ for c in found.partition.sizes()])
+    for C_ in (1536, 3584, 5632):
+        pred = kv.simulate_ttft(kv.Strategy.KVR, kv.partition_from_table(t, C_), m, kv.CostModel(), kv.NetworkModel())
+        fresh = kv.search_partition(C_, 4, m, kv.CostModel(), kv.NetworkModel())
+        assert (pred - fresh.ttft) / fresh.ttft <= 0.05
+
+
+@pytest.mark.skipif(not O.Reference.available(), reason="oracle/_ref not built")
+def test_noise_and_table_bit_exact_vs_reference():
+    ref = O.Reference()
+    rng = np.random.default_rng(17)
+    for _ in range(30):
+        p = int(rng.integers(2, 7))
+        C_ = p * 8 + int(rng.integers(0, 5000))
+        b = kv.even_partition(C_, p)
+        for s in (kv.Strategy.KVR, kv.Strategy.TSP):
+            factor = float(2.0 ** rng.integers(0, 12))
+            got = kv.noise_study(s, b, kv.ModelConfig(n_layers=3), kv.CostModel(), kv.NetworkModel(), factor, 7, 11)
+            exp = ref.noise_study(int(s), b.boundaries, 3, factor, 7, 11)
+            assert (got.quiet_ttft, got.mean_degradation, got.max_degradation, got.per_trial) == exp
+        entries = {}
+        for _k in range(int(rng.integers(1, 5))):
+            r = rng.random(p) + 0.01
+            entries[int(rng.integers(1, 20000))] = (r / r.sum()).tolist()
+        t = kv.PartitionLookupTable(p)
+        for k, v in entries.items():
+            t.insert(k, v)
+        q = int(rng.integers(p, 25000))
+        r_ref, b_ref = ref.table(entries, p, q)
+        assert kv.interpolate_partition(t, q) == r_ref
+        assert kv.partition_from_table(t, q).boundaries == b_ref
