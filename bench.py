@@ -376,7 +376,7 @@ def main():
 
     # profiled pass: per-kernel-class device time (events on the launching stream)
     W.set_profiling(True)
-    step_device()
+    prof_ttft, _ = step_device()
     stats = W.kernel_stats()
     W.set_profiling(False)
     peaks = load_peaks()
@@ -428,6 +428,7 @@ def main():
             "wall_s_timed": wall,
             "roofline": roofline,
             "kernels": kernels,
+            "profiled_step": {"ttft_ms": prof_ttft, "kernel_sum_ms": sum(v["total_ms"] for v in stats.values())},
             "clocks": clk.summary(),
             "gpu_launches": launches,
             "e2e": e2e}

@@ -33,7 +33,7 @@ namespace {
 
 constexpr int BQ = 128;   // queries per tile (two tiles per CTA)
 constexpr int BKV = 128;  // keys per tile
-constexpr int THREADS = 320;
+constexpr int THREADS = 576;  // warp 0 TMA, warp 1 MMA, warps 2..17 softmax (8 per query tile)
 constexpr uint32_t TMEM_COLS = 512;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units: p <= 2^8 between rescales
 
@@ -42,7 +42,7 @@ struct ACfg {
     static constexpr int HALVES = HD / 64;  // 64-wide (128 B) TMA boxes
     static constexpr uint32_t Q_BYTES = BQ * HD * 2;
     static constexpr uint32_t KV_BYTES = BKV * HD * 2;
-    static constexpr uint32_t SMEM = 2 * Q_BYTES + 4 * KV_BYTES + 1024 + 256;
+    static constexpr uint32_t SMEM = 2 * Q_BYTES + 4 * KV_BYTES + 1024 + 256 + 6144;  // + row-max/sum exchange
 };
 
 // ---- packed f32x2 arithmetic (sm_100: FFMA2 / FADD2) and exp2 on two pipes ----
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             ptx::mbar_init(&v_full[s], 1);
             ptx::mbar_init(&kv_empty[s], 1);
             ptx::mbar_init(&s_full[s], 1);
-            ptx::mbar_init(&p_full[s], 4);
+            ptx::mbar_init(&p_full[s], 8);
             ptx::mbar_init(&o_done[s], 1);
         }
         ptx::fence_barrier_init();
@@ -223,41 +223,55 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     } else {
-        const int x = (warp - 2) >> 2;      // query tile of this warpgroup
-        const uint32_t quarter = warp & 3;  // TMEM lane quarter this warp may access
-        const int64_t row = q0 + x * BQ + quarter * 32 + lane;
+        // 16 softmax warps: 8 per query tile; the two warps of a TMEM lane quarter split the
+        // tile's 128 key columns (and the O columns) and exchange row max / row sum through smem.
+        const int sw = warp - 2;
+        const int x = sw >> 3;                // query tile
+        const int sub = (sw >> 2) & 1;        // key half (and O half) of this warp
+        const uint32_t quarter = warp & 3;    // TMEM lane quarter this warp may access
+        constexpr int KC = BKV / 2, OC = HD / 2;
+        const int xrow = static_cast<int>(quarter) * 32 + lane;
+        const int64_t row = q0 + x * BQ + xrow;
         const int64_t abs_row = a.offset + row;
         const uint32_t lane_base = tmem + ((quarter * 32u) << 16);
-        const uint32_t s_col = x * 128, o_col = 256 + x * 128;
+        const uint32_t s_col = x * 128 + sub * KC;        // fp32 S columns of my key half
+        const uint32_t p_col = x * 128 + sub * (KC / 2);  // packed bf16 P columns of my key half
+        const uint32_t o_col = 256 + x * 128 + sub * OC;
+        float* xch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bar) + 256);  // [2 par][2 x][2 sub][128]
+        const uint32_t bar_id = 1 + x * 4 + quarter;      // named barrier of the two partner warps
         const int nt = n_kt[x];
         const int64_t tile_first_abs = a.offset + q0 + x * BQ;
         float m_run = -INFINITY, l = 0.f;
         for (int j = 0; j < nt; ++j) {
             ptx::mbar_wait(&s_full[x], j & 1);
             ptx::tc_fence_after();
-            float sv[BKV];
+            float sv[KC];
 #pragma unroll
-            for (int c = 0; c < BKV / 32; ++c) {
+            for (int c = 0; c < KC / 32; ++c) {
                 uint32_t r[32];
                 ptx::tmem_ld32(lane_base + s_col + c * 32, r);
                 ptx::tmem_ld_wait();
 #pragma unroll
                 for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(r[i]);
             }
-            const int64_t key0 = static_cast<int64_t>(j) * BKV;
-            const bool diag = key0 + BKV - 1 > tile_first_abs;  // tile crosses the causal diagonal
+            const int64_t key0 = static_cast<int64_t>(j) * BKV + sub * KC;  // first key of my half
+            const bool diag = static_cast<int64_t>(j) * BKV + BKV - 1 > tile_first_abs;
             if (diag) {
                 // keys [key0, key0 + nvis) are visible to this row; 32-bit compares against
                 // compile-time column indices, applied only on the diagonal tile
                 const int64_t v = abs_row - key0 + 1;
-                const int nvis = v < 0 ? 0 : (v > BKV ? BKV : static_cast<int>(v));
+                const int nvis = v < 0 ? 0 : (v > KC ? KC : static_cast<int>(v));
 #pragma unroll
-                for (int i = 0; i < BKV; ++i) sv[i] = i < nvis ? sv[i] : -INFINITY;
+                for (int i = 0; i < KC; ++i) sv[i] = i < nvis ? sv[i] : -INFINITY;
             }
             float mx = -INFINITY;
 #pragma unroll
-            for (int i = 0; i < BKV; ++i) mx = fmaxf(mx, sv[i]);
-            mx *= a.sl2;  // scale > 0: max commutes with it
+            for (int i = 0; i < KC; ++i) mx = fmaxf(mx, sv[i]);
+            float* xb = xch + (j & 1) * 512 + x * 256;
+            xb[sub * 128 + xrow] = mx;
+            asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+            mx = fmaxf(mx, xb[(sub ^ 1) * 128 + xrow]);  // row max over all 128 keys
+            mx *= a.sl2;                                   // scale > 0: max commutes with it
             const bool need = mx > m_run + RESCALE_THRESHOLD;
             if (__any_sync(0xffffffffu, need)) {
                 const float m_new = need ? mx : m_run;
@@ -266,7 +280,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     ptx::mbar_wait(&o_done[x], (j - 1) & 1);
                     ptx::tc_fence_after();
 #pragma unroll
-                    for (int c = 0; c < HD / 16; ++c) {
+                    for (int c = 0; c < OC / 16; ++c) {
                         uint32_t r[16];
                         ptx::tmem_ld16(lane_base + o_col + c * 16, r);
                         ptx::tmem_ld_wait();
@@ -283,28 +297,28 @@ __global__ void __launch_bounds__(THREADS, 1)
             const float2 sl2v = make_float2(a.sl2, a.sl2), nb2 = make_float2(nbv, nbv);
             float2 lacc = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int c = 0; c < BKV / 32; ++c) {
+            for (int c = 0; c < KC / 32; ++c) {
                 uint32_t pk[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const int col = c * 32 + 2 * i;
-                    // the exp2 unit is chosen by key column only: deterministic per (row, key)
+                    const int gcol = sub * KC + col;  // the exp2 unit depends on the key column only
                     const float2 xv = ffma2(make_float2(sv[col], sv[col + 1]), sl2v, nb2);
                     float2 pv;
-                    if (col >= POLY_FROM) {
+                    if (gcol >= POLY_FROM) {
                         pv = ex2_poly2(xv);
+                        if (diag) {  // the FMA-pipe exp2 clamps -inf: zero masked keys
+                            pv.x = sv[col] == -INFINITY ? 0.f : pv.x;
+                            pv.y = sv[col + 1] == -INFINITY ? 0.f : pv.y;
+                        }
                     } else {
                         pv.x = ex2_mufu(xv.x);
                         pv.y = ex2_mufu(xv.y);
                     }
-                    if (col >= POLY_FROM && diag) {  // the FMA-pipe exp2 clamps -inf: zero masked keys
-                        pv.x = sv[col] == -INFINITY ? 0.f : pv.x;
-                        pv.y = sv[col + 1] == -INFINITY ? 0.f : pv.y;
-                    }
                     lacc = fadd2(lacc, pv);
                     pk[i] = ptx::pack_bf16(pv.x, pv.y);
                 }
-                ptx::tmem_st16(lane_base + s_col + c * 16, pk);  // P over S, packed bf16
+                ptx::tmem_st16(lane_base + p_col + c * 16, pk);  // P over S, packed bf16
             }
             l += lacc.x + lacc.y;
             ptx::tmem_st_wait();
@@ -312,13 +326,17 @@ __global__ void __launch_bounds__(THREADS, 1)
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&p_full[x]);
         }
-        // epilogue: O / l -> bf16
+        // epilogue: O / (l_0 + l_1) -> bf16, each warp its O half
+        float* lb = xch + 1024 + x * 256;
+        lb[sub * 128 + xrow] = l;
+        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+        const float lo = lb[xrow], hi = lb[128 + xrow];
+        const float inv = 1.0f / (lo + hi);  // same order on both partners
         ptx::mbar_wait(&o_done[x], (nt - 1) & 1);
         ptx::tc_fence_after();
-        const float inv = 1.0f / l;
-        bf16* orow = a.O + row * a.ldo + static_cast<int64_t>(h) * HD;
+        bf16* orow = a.O + row * a.ldo + static_cast<int64_t>(h) * HD + sub * OC;
 #pragma unroll
-        for (int c = 0; c < HD / 32; ++c) {
+        for (int c = 0; c < OC / 32; ++c) {
             uint32_t r[32];
             ptx::tmem_ld32(lane_base + o_col + c * 32, r);
             ptx::tmem_ld_wait();

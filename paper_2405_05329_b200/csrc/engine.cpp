@@ -22,6 +22,7 @@
 #include <condition_variable>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <deque>
 #include <memory>
 #include <mutex>
@@ -339,6 +340,10 @@ struct RankCtx {
         cudaEvent_t a, b;
     };
     bool profiling = false;
+    // CUDA graph of a single-rank prefill (all layers), keyed by shape + buffer identity
+    cudaGraphExec_t graph = nullptr;
+    uint64_t graph_key = 0;
+    int64_t graph_launches = 0;
     std::vector<Mark> marks;
     std::vector<cudaEvent_t> pool;
     size_t pool_used = 0;
@@ -390,6 +395,9 @@ struct RankCtx {
             for (auto e : *v) cudaEventDestroy(e);
             v->clear();
         }
+        if (graph) cudaGraphExecDestroy(graph);
+        graph = nullptr;
+        graph_key = 0;
         for (auto ev : pool) cudaEventDestroy(ev);
         pool.clear();
         pool_used = 0;
@@ -660,6 +668,50 @@ static void run_engine(kvp_engine* e, int32_t strategy, const float* ctx, int64_
         const size_t row_kv = static_cast<size_t>(s.kv) * es;
         KVP_CUDA(cudaEventRecord(R.ev_begin, R.comp));
         KVP_CUDA(cudaMemcpyAsync(R.h.p, ctx + start * s.d, c * s.d * 4, cudaMemcpyDefault, R.comp));
+        // Single-rank prefill (serial / KVR p=1): no cross-rank protocol inside the layer loop,
+        // so the 5L kernels + timing events are captured once into a CUDA graph and replayed
+        // (removes per-launch host and GPU front-end gaps).  KVP_GRAPH=0 disables.
+        static const bool use_graph = [] {
+            const char* g = getenv("KVP_GRAPH");
+            return !(g && g[0] == '0');
+        }();
+        if (p == 1 && strategy != KVP_TSP && use_graph && !R.profiling) {
+            const uint64_t key = (static_cast<uint64_t>(c) << 20) ^ (reinterpret_cast<uintptr_t>(R.h.p) >> 4) ^
+                                 (reinterpret_cast<uintptr_t>(R.kv.p) << 7) ^ (reinterpret_cast<uintptr_t>(R.x.p) << 13) ^
+                                 static_cast<uint64_t>(strategy);
+            if (!R.graph || R.graph_key != key) {
+                if (R.graph) cudaGraphExecDestroy(R.graph);
+                R.graph = nullptr;
+                const int64_t l0 = launch_count();
+                cudaGraph_t g = nullptr;
+                KVP_CUDA(cudaStreamBeginCapture(R.comp, cudaStreamCaptureModeThreadLocal));
+                for (int64_t l = 0; l < s.L; ++l) {
+                    const LayerW& w = e->weights[static_cast<size_t>(slot)]->layers[static_cast<size_t>(l)];
+                    uint8_t* K = static_cast<uint8_t*>(R.kv_ptr(s, l, 0));
+                    uint8_t* V = static_cast<uint8_t*>(R.kv_ptr(s, l, 1));
+                    KVP_CUDA(cudaEventRecord(R.t_start[l], R.comp));
+                    exec_qkv(s, w, R, c, K, V, l == 0);
+                    KVP_CUDA(cudaEventRecord(R.t_qkv[l], R.comp));
+                    KVP_CUDA(cudaEventRecord(R.t_attn[l], R.comp));
+                    exec_finish(s, w, R, c, K, V, c, 0);
+                    KVP_CUDA(cudaEventRecord(R.t_end[l], R.comp));
+                }
+                KVP_CUDA(cudaStreamEndCapture(R.comp, &g));
+                KVP_CUDA(cudaGraphInstantiate(&R.graph, g, 0));
+                cudaGraphDestroy(g);
+                R.graph_key = key;
+                R.graph_launches = launch_count() - l0;
+            } else {
+                for (int64_t i = 0; i < R.graph_launches; ++i) note_launch();
+            }
+            KVP_CUDA(cudaGraphLaunch(R.graph, R.comp));
+            for (int64_t l = 0; l < s.L; ++l) m.dots[0] += c * c;
+            if (ft) KVP_CUDA(cudaMemcpyAsync(ft, R.h.as<float>() + (c - 1) * s.d, s.d * 4, cudaMemcpyDefault, R.comp));
+            KVP_CUDA(cudaEventRecord(R.ev_done, R.comp));
+            if (hid) KVP_CUDA(cudaMemcpyAsync(hid, R.h.p, c * s.d * 4, cudaMemcpyDefault, R.comp));
+            fab.close_from(r);
+            return;
+        }
         for (int64_t l = 0; l < s.L; ++l) {
             const LayerW& w = e->weights[static_cast<size_t>(slot)]->layers[static_cast<size_t>(l)];
             uint8_t* K = static_cast<uint8_t*>(R.kv_ptr(s, l, 0));

@@ -14,8 +14,11 @@ shapes = {  # name: (M, N, K, epi)
     "p8_ffn2": (512, 4096, 8192, 1), "falcon_qkv": (8192, 4672, 4544, 0), "falcon_o": (8192, 4544, 4544, 1),
     "sq8192": (8192, 8192, 8192, 3),
 }
+only = set(sys.argv[1:])
 out = {}
 for name, (M, N, K, epi) in shapes.items():
+    if only and name not in only:
+        continue
     ms, tf, bn = W.bench_gemm(M, N, K, epi, 20)
     out[name] = {"M": M, "N": N, "K": K, "epi": epi, "ms": ms, "tflops": tf, "bn": bn}
     print(json.dumps({name: out[name]}), flush=True)
