@@ -201,6 +201,32 @@ __device__ __forceinline__ float store_chunk(const EpiArgs& ep, int64_t row, int
     return ss;
 }
 
+// EPI_RESID with the residual already in registers (prefetched before the accumulator was
+// ready): out = resid + acc (f32), bf16 copy, sum of squares.
+__device__ __forceinline__ float store_resid_prefetched(const EpiArgs& ep, int64_t row, int64_t col0,
+                                                        const uint32_t (&r)[32], const float4 (&rv)[8]) {
+    float* o = ep.outf + row * ep.ldf + col0;
+    bf16* ob = ep.outb ? ep.outb + row * ep.ldb + col0 : nullptr;
+    float ss = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        float4 v;
+        v.x = rv[j].x + __uint_as_float(r[4 * j + 0]);
+        v.y = rv[j].y + __uint_as_float(r[4 * j + 1]);
+        v.z = rv[j].z + __uint_as_float(r[4 * j + 2]);
+        v.w = rv[j].w + __uint_as_float(r[4 * j + 3]);
+        *reinterpret_cast<float4*>(o + 4 * j) = v;
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+        if (ob) {
+            uint2 pk;
+            pk.x = ptx::pack_bf16(v.x, v.y);
+            pk.y = ptx::pack_bf16(v.z, v.w);
+            *reinterpret_cast<uint2*>(ob + 4 * j) = pk;
+        }
+    }
+    return ss;
+}
+
 template <int BN, int KIND>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
@@ -299,35 +325,64 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
             const int m_blk = tile % num_m, n_blk = tile / num_m;
             const uint32_t buf = t & 1, aphase = (t >> 1) & 1;
-            ptx::mbar_wait(&tfull[buf], aphase);
-            ptx::tc_fence_after();
             const int64_t row = static_cast<int64_t>(m_blk) * BM + quarter * 32 + lane;
             const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + buf * BN;
-            float row_scale = 1.f;
-            if constexpr (KIND != EPI_RESID) {
+            float ssacc = 0.f;
+            if constexpr (KIND == EPI_RESID) {
+                // The residual does not depend on the accumulator: fetch two chunks of it while
+                // the tile's MMAs are still running, then keep two chunks in flight.
+                float4 rv[8];
+                auto fetch = [&](int cc) {
+                    const int64_t col0 = static_cast<int64_t>(n_blk) * BN + (half * MY + cc) * 32;
+                    if (row < M && col0 + 32 <= N) {
+                        const float4* src = reinterpret_cast<const float4*>(ep.resid + row * ep.ldr + col0);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) rv[j] = src[j];
+                    }
+                };
+                fetch(0);
+                ptx::mbar_wait(&tfull[buf], aphase);
+                ptx::tc_fence_after();
+#pragma unroll
+                for (int cc = 0; cc < MY; ++cc) {
+                    const int c = half * MY + cc;
+                    const int64_t col0 = static_cast<int64_t>(n_blk) * BN + c * 32;
+                    if (col0 >= N) break;  // warp-uniform
+                    uint32_t r[32];
+                    ptx::tmem_ld32(taddr + c * 32, r);
+                    ptx::tmem_ld_wait();
+                    if (row < M) {
+                        if (col0 + 32 <= N)
+                            ssacc += store_resid_prefetched(ep, row, col0, r, rv);
+                        else
+                            ssacc += store_chunk<KIND>(ep, row, col0, N, r, 1.f);
+                    }
+                    if (cc + 1 < MY) fetch(cc + 1);
+                    // one partial per 64-column group, independent of BN and of the warp split
+                    if (ep.ssq_out != nullptr && row < M && (((c + 1) & 1) == 0 || col0 + 32 >= N)) {
+                        ep.ssq_out[row * ep.ssq_parts + (col0 >> 6)] = ssacc;
+                        ssacc = 0.f;
+                    }
+                }
+            } else {
+                ptx::mbar_wait(&tfull[buf], aphase);
+                ptx::tc_fence_after();
+                float row_scale = 1.f;
                 if (ep.ssq_in != nullptr && row < M) {
                     const float* sp = ep.ssq_in + row * ep.ssq_parts;
                     float ss = 0.f;
                     for (int q = 0; q < ep.ssq_parts; ++q) ss += sp[q];
                     row_scale = 1.0f / sqrtf(ss * ep.inv_norm_cols + 1e-6f);
                 }
-            }
-            float ssacc = 0.f;
 #pragma unroll 1
-            for (int cc = 0; cc < MY; ++cc) {
-                const int c = half * MY + cc;
-                const int64_t col0 = static_cast<int64_t>(n_blk) * BN + c * 32;
-                if (col0 >= N) break;  // warp-uniform
-                uint32_t r[32];
-                ptx::tmem_ld32(taddr + c * 32, r);
-                ptx::tmem_ld_wait();
-                if (row < M) ssacc += store_chunk<KIND>(ep, row, col0, N, r, row_scale);
-                if constexpr (KIND == EPI_RESID) {
-                    // one partial per 64-column group, independent of BN and of the warp split
-                    if (ep.ssq_out != nullptr && row < M && (((c + 1) & 1) == 0 || col0 + 32 >= N)) {
-                        ep.ssq_out[row * ep.ssq_parts + (col0 >> 6)] = ssacc;
-                        ssacc = 0.f;
-                    }
+                for (int cc = 0; cc < MY; ++cc) {
+                    const int c = half * MY + cc;
+                    const int64_t col0 = static_cast<int64_t>(n_blk) * BN + c * 32;
+                    if (col0 >= N) break;  // warp-uniform
+                    uint32_t r[32];
+                    ptx::tmem_ld32(taddr + c * 32, r);
+                    ptx::tmem_ld_wait();
+                    if (row < M) store_chunk<KIND>(ep, row, col0, N, r, row_scale);
                 }
             }
             ptx::tc_fence_before();
