@@ -91,8 +91,8 @@ __global__ void __launch_bounds__(THREADS) attn_mma_kernel(const bf16* __restric
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int num_qt = static_cast<int>((sh.q_rows + BLOCK_M - 1) / BLOCK_M);
-    const int qt = num_qt - 1 - static_cast<int>(blockIdx.x);  // heaviest tiles first
-    const int h = blockIdx.y;
+    const int qt = num_qt - 1 - static_cast<int>(blockIdx.y);  // heaviest tiles (all heads) first
+    const int h = blockIdx.x;
     const int g = h / (sh.n_heads / sh.n_kv_heads);
     const int64_t q0 = static_cast<int64_t>(qt) * BLOCK_M;
     const int64_t last_q = (q0 + BLOCK_M - 1 < sh.q_rows - 1) ? q0 + BLOCK_M - 1 : sh.q_rows - 1;
@@ -246,7 +246,7 @@ void launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShap
         cudaFuncSetAttribute(attn_mma_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         configured = dev;
     }
-    dim3 grid(static_cast<unsigned>((sh.q_rows + BLOCK_M - 1) / BLOCK_M), static_cast<unsigned>(sh.n_heads));
+    dim3 grid(static_cast<unsigned>(sh.n_heads), static_cast<unsigned>((sh.q_rows + BLOCK_M - 1) / BLOCK_M));
     note_launch();
     attn_mma_kernel<HD><<<grid, THREADS, smem, s>>>(Q, K, V, O, sh);
 }

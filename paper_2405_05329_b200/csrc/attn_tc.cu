@@ -120,8 +120,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int num_pairs = static_cast<int>((a.q_rows + 2 * BQ - 1) / (2 * BQ));
-    const int pair = num_pairs - 1 - static_cast<int>(blockIdx.x);  // heaviest first
-    const int h = blockIdx.y;
+    // grid = (heads, pairs): the block scheduler walks x fastest, so ALL heads of the heaviest
+    // (latest) query pair are dispatched first -- a global longest-first order over the causal
+    // work imbalance
+    const int pair = num_pairs - 1 - static_cast<int>(blockIdx.y);
+    const int h = blockIdx.x;
     const int g = h / a.group;
     const int64_t q0 = static_cast<int64_t>(pair) * 2 * BQ;
     // key tiles needed by each query tile (tile b covers tile a's range plus one)
@@ -378,7 +381,7 @@ void launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShap
     }
     AttnArgs a{sh.q_rows, sh.k_rows, sh.offset, sh.n_heads, sh.n_heads / sh.n_kv_heads, sh.ldo, O,
                (1.0f / sqrtf(static_cast<float>(HD))) * 1.4426950408889634f};
-    dim3 grid(static_cast<unsigned>((sh.q_rows + 2 * BQ - 1) / (2 * BQ)), static_cast<unsigned>(sh.n_heads));
+    dim3 grid(static_cast<unsigned>(sh.n_heads), static_cast<unsigned>((sh.q_rows + 2 * BQ - 1) / (2 * BQ)));
     note_launch();
     attn_tc_kernel<HD, POLY_FROM><<<grid, THREADS, ACfg<HD>::SMEM, s>>>(tq, tk, tv, a);
 }
