@@ -229,8 +229,8 @@ __device__ __forceinline__ float store_resid_prefetched(const EpiArgs& ep, int64
 
 template <int BN, int KIND>
 __global__ void __launch_bounds__(THREADS, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int K, EpiArgs ep) {
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmBh, int M, int N, int K, int n_full, EpiArgs ep) {
     using C = Cfg<BN>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -244,12 +244,28 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
-    const int num_tiles = num_m * num_n;
+    // Tiles [0, n_full) are BN wide; the remaining (last partial wave of) BN tiles run as two
+    // BN/2-wide tiles each so the persistent grid's final round is evenly filled.  Only the
+    // tile width changes, not the per-element K order: results are identical either way.
+    const int num_tiles = n_full + 2 * (num_m * num_n - n_full);
+    auto decode = [&](int tile, int& m_blk, int& col_base, int& width) {
+        if (tile < n_full) {
+            m_blk = tile % num_m;
+            col_base = (tile / num_m) * BN;
+            width = BN;
+        } else {
+            const int k = tile - n_full, big = n_full + (k >> 1);
+            m_blk = big % num_m;
+            col_base = (big / num_m) * BN + (k & 1) * (BN / 2);
+            width = BN / 2;
+        }
+    };
     const int num_kb = (K + BK - 1) / BK;
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmA);
         ptx::tma_prefetch_desc(&tmB);
+        ptx::tma_prefetch_desc(&tmBh);
         for (int s = 0; s < STAGES; ++s) {
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], 1);
@@ -271,12 +287,14 @@ __global__ void __launch_bounds__(THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                const int m_blk = tile % num_m, n_blk = tile / num_m;
+                int m_blk, col_base, width;
+                decode(tile, m_blk, col_base, width);
+                const bool narrow = width != BN;
                 for (int kb = 0; kb < num_kb; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    ptx::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+                    ptx::mbar_arrive_expect_tx(&full[stage], C::A_BYTES + (narrow ? C::B_BYTES / 2 : C::B_BYTES));
                     ptx::tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
-                    ptx::tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN);
+                    ptx::tma_load_2d(sB + stage * C::B_BYTES, narrow ? &tmBh : &tmB, &full[stage], kb * BK, col_base);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -286,11 +304,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            constexpr uint32_t idesc = ptx::idesc_bf16(BM, BN);
+            constexpr uint32_t idesc_w = ptx::idesc_bf16(BM, BN), idesc_n = ptx::idesc_bf16(BM, BN / 2);
             int stage = 0;
             uint32_t phase = 0;
             int t = 0;
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+                int m_blk_u, col_base_u, width;
+                decode(tile, m_blk_u, col_base_u, width);
+                const uint32_t idesc = width == BN ? idesc_w : idesc_n;
                 const uint32_t buf = t & 1, aphase = (t >> 1) & 1;
                 ptx::mbar_wait(&tempty[buf], aphase ^ 1);
                 ptx::tc_fence_after();
@@ -320,10 +341,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         // warps of a lane quarter split the tile's columns (more loads in flight per row).
         const uint32_t quarter = warp & 3;
         const int half = (warp - 2) >> 2;
-        constexpr int CHUNKS = BN / 32, MY = CHUNKS / 2;
+        constexpr int MY_MAX = BN / 64;  // 32-column chunks per warp group on a full-width tile
         int t = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
-            const int m_blk = tile % num_m, n_blk = tile / num_m;
+            int m_blk, col_base, width;
+            decode(tile, m_blk, col_base, width);
+            const int MY = width / 64;
             const uint32_t buf = t & 1, aphase = (t >> 1) & 1;
             const int64_t row = static_cast<int64_t>(m_blk) * BM + quarter * 32 + lane;
             const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + buf * BN;
@@ -333,7 +356,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 // the tile's MMAs are still running, then keep two chunks in flight.
                 float4 rv[8];
                 auto fetch = [&](int cc) {
-                    const int64_t col0 = static_cast<int64_t>(n_blk) * BN + (half * MY + cc) * 32;
+                    const int64_t col0 = static_cast<int64_t>(col_base) + (half * MY + cc) * 32;
                     if (row < M && col0 + 32 <= N) {
                         const float4* src = reinterpret_cast<const float4*>(ep.resid + row * ep.ldr + col0);
 #pragma unroll
@@ -344,9 +367,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                 ptx::mbar_wait(&tfull[buf], aphase);
                 ptx::tc_fence_after();
 #pragma unroll
-                for (int cc = 0; cc < MY; ++cc) {
+                for (int cc = 0; cc < MY_MAX; ++cc) {
+                    if (cc >= MY) break;
                     const int c = half * MY + cc;
-                    const int64_t col0 = static_cast<int64_t>(n_blk) * BN + c * 32;
+                    const int64_t col0 = static_cast<int64_t>(col_base) + c * 32;
                     if (col0 >= N) break;  // warp-uniform
                     uint32_t r[32];
                     ptx::tmem_ld32(taddr + c * 32, r);
@@ -377,7 +401,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll 1
                 for (int cc = 0; cc < MY; ++cc) {
                     const int c = half * MY + cc;
-                    const int64_t col0 = static_cast<int64_t>(n_blk) * BN + c * 32;
+                    const int64_t col0 = static_cast<int64_t>(col_base) + c * 32;
                     if (col0 >= N) break;  // warp-uniform
                     uint32_t r[32];
                     ptx::tmem_ld32(taddr + c * 32, r);
@@ -399,8 +423,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 template <int BN, int KIND>
-void launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const EpiArgs& ep,
-               cudaStream_t s) {
+void launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tbh, int M, int N, int K,
+               const EpiArgs& ep, cudaStream_t s) {
     auto kern = gemm_tc_kernel<BN, KIND>;
     static thread_local int configured_dev = -1;
     int dev = 0;
@@ -410,21 +434,29 @@ void launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K
         configured_dev = dev;
     }
     const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-    const int grid = tiles < num_sms() ? tiles : num_sms();
+    const int sms = num_sms();
+    const int grid = tiles < sms ? tiles : sms;
+    // split the last partial round into half-width tiles when they fit in one round
+    static const bool split_tail = [] {
+        const char* e = getenv("KVP_GEMM_TAIL");
+        return !(e && e[0] == '0');
+    }();
+    const int rem = tiles % grid;
+    const int n_full = (split_tail && BN == 256 && tiles > grid && rem > 0 && 2 * rem <= grid) ? tiles - rem : tiles;
     note_launch();
-    kern<<<grid, THREADS, Cfg<BN>::SMEM, s>>>(ta, tb, M, N, K, ep);
+    kern<<<grid, THREADS, Cfg<BN>::SMEM, s>>>(ta, tb, tbh, M, N, K, n_full, ep);
 }
 
 template <int BN>
-void dispatch(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const GemmEpilogue& g,
-              cudaStream_t s) {
+void dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tbh, int M, int N, int K,
+              const GemmEpilogue& g, cudaStream_t s) {
     EpiArgs ep{g.out0, g.ld0, g.n0, g.out1, g.ld1, g.n1, g.out2, g.ld2, g.outf, g.ldf, g.resid, g.ldr,
                g.outb, g.ldb, g.ssq_out, g.ssq_in, g.ssq_parts, g.norm_cols ? 1.0f / static_cast<float>(g.norm_cols) : 0.f};
     switch (g.kind) {
-        case EPI_QKV: launch_tc<BN, EPI_QKV>(ta, tb, M, N, K, ep, s); break;
-        case EPI_RESID: launch_tc<BN, EPI_RESID>(ta, tb, M, N, K, ep, s); break;
-        case EPI_RELU: launch_tc<BN, EPI_RELU>(ta, tb, M, N, K, ep, s); break;
-        default: launch_tc<BN, EPI_STORE>(ta, tb, M, N, K, ep, s); break;
+        case EPI_QKV: launch_tc<BN, EPI_QKV>(ta, tb, tbh, M, N, K, ep, s); break;
+        case EPI_RESID: launch_tc<BN, EPI_RESID>(ta, tb, tbh, M, N, K, ep, s); break;
+        case EPI_RELU: launch_tc<BN, EPI_RELU>(ta, tb, tbh, M, N, K, ep, s); break;
+        default: launch_tc<BN, EPI_STORE>(ta, tb, tbh, M, N, K, ep, s); break;
     }
 }
 
@@ -460,17 +492,18 @@ void gemm_bf16_tc(const bf16* A, int64_t M, int64_t K, const bf16* B, int64_t N,
         throw std::runtime_error("gemm_bf16_tc: K must be a multiple of 8 and operands 16-byte aligned");
     const int BN = gemm_bf16_tc_bn(M, N);
     const bool wide = BN == 256;
-    CUtensorMap ta, tb;
-    if (!make_tmap_bf16(&ta, A, K, M, K, BK, BM) || !make_tmap_bf16(&tb, B, K, N, K, BK, BN)) {
+    CUtensorMap ta, tb, tbh;
+    if (!make_tmap_bf16(&ta, A, K, M, K, BK, BM) || !make_tmap_bf16(&tb, B, K, N, K, BK, BN) ||
+        !make_tmap_bf16(&tbh, B, K, N, K, BK, BN / 2)) {
         char msg[160];
         snprintf(msg, sizeof msg, "cuTensorMapEncodeTiled failed (M=%lld N=%lld K=%lld)", (long long)M,
                  (long long)N, (long long)K);
         throw std::runtime_error(msg);
     }
     if (wide)
-        dispatch<256>(ta, tb, (int)M, (int)N, (int)K, ep, s);
+        dispatch<256>(ta, tb, tbh, (int)M, (int)N, (int)K, ep, s);
     else
-        dispatch<128>(ta, tb, (int)M, (int)N, (int)K, ep, s);
+        dispatch<128>(ta, tb, tbh, (int)M, (int)N, (int)K, ep, s);
 }
 
 }  // namespace kvp
