@@ -231,6 +231,17 @@ kvp_status kvp_search_partition(int64_t C, int64_t p, int64_t n_layers, const kv
 /* practical_bound (simnet.hpp:297-316). */
 kvp_status kvp_practical_bound(int64_t C, int64_t p, int64_t n_layers, const kvp_cost_model* cost,
                                int64_t* boundaries_out, double* ttft_out);
+/* Extension (not in the reference): simulate_ttft with the attention term priced on the
+ * CAUSAL-VISIBLE pairs the B200 kernels actually compute -- alpha * c_i * (b_i + (c_i+1)/2) for
+ * both KVR and TSP (tile-skipping) -- instead of the reference's alpha*c_i*b_{i+1} (KVR) and
+ * dense alpha*c_i*C (TSP).  Everything else (projection, softmax, wire, barriers) unchanged.
+ * kvp_search_partition_causal = the grid search scored by it. */
+kvp_status kvp_simulate_ttft_causal(int32_t strategy, int64_t C, const int64_t* boundaries, int64_t p,
+                                    int64_t n_layers, const kvp_cost_model* cost, const kvp_network_model* net,
+                                    double* ttft_out);
+kvp_status kvp_search_partition_causal(int64_t C, int64_t p, int64_t n_layers, const kvp_cost_model* cost,
+                                       const kvp_network_model* net, const kvp_search_config* cfg,
+                                       int64_t* boundaries_out, kvp_search_result* res);
 /* simulate_ttft with a NoiseSidecar{seed, slowdown_factor} (simnet.hpp:65-78,136-141). */
 kvp_status kvp_simulate_ttft_noisy(int32_t strategy, int64_t C, const int64_t* boundaries, int64_t p,
                                    int64_t n_layers, const kvp_cost_model* cost, const kvp_network_model* net,

@@ -102,6 +102,7 @@ struct Noise {
     bool on = false;
     uint64_t seed = 1;
     double factor = 1.0;
+    bool causal = false;  // extension: price attention on causal-visible pairs (B200 kernels)
 };
 
 static uint64_t sm_next(uint64_t& s) {
@@ -146,7 +147,9 @@ double simulate(int32_t strategy, int64_t C, const int64_t* b, int64_t p, int64_
             const double released = gather + rounds * worst;
             for (int64_t i = 0; i < p; ++i) {
                 const int64_t c = b[i + 1] - b[i];
-                const double attn = cost.alpha * static_cast<double>(c) * static_cast<double>(C);
+                const double pairs = nz.causal ? static_cast<double>(b[i]) + 0.5 * static_cast<double>(c + 1)
+                                               : static_cast<double>(C);
+                const double attn = cost.alpha * static_cast<double>(c) * pairs;
                 t[static_cast<size_t>(i)] = released + attn + cost.softmax_coeff * static_cast<double>(c) + cost.fixed_overhead;
             }
         } else {
@@ -162,7 +165,9 @@ double simulate(int32_t strategy, int64_t C, const int64_t* b, int64_t p, int64_
                     up_start = ready;
                     up_wire = w;
                 }
-                const double attn_end = ready + cost.alpha * static_cast<double>(c) * static_cast<double>(held);
+                const double pairs = nz.causal ? static_cast<double>(b[i]) + 0.5 * static_cast<double>(c + 1)
+                                               : static_cast<double>(held);
+                const double attn_end = ready + cost.alpha * static_cast<double>(c) * pairs;
                 double end = attn_end + cost.softmax_coeff * static_cast<double>(c) + cost.fixed_overhead;
                 if (i + 1 < p) end = std::max(end, sent);
                 t[static_cast<size_t>(i)] = end;
@@ -311,11 +316,14 @@ struct SimUser {
     int64_t L;
     kvp_cost_model cost;
     kvp_network_model net;
+    bool causal = false;
 };
 
 static double sim_eval(const int64_t* b, int64_t p, void* u) {
     const SimUser* s = static_cast<const SimUser*>(u);
-    return simulate(KVP_KVR, b[p], b, p, s->L, s->cost, s->net);
+    Noise nz;
+    nz.causal = s->causal;
+    return simulate(KVP_KVR, b[p], b, p, s->L, s->cost, s->net, nz);
 }
 
 // Least squares with non-negativity by active-set elimination over <= 3 unknowns.
@@ -491,6 +499,35 @@ kvp_status kvp_practical_bound(int64_t C, int64_t p, int64_t L, const kvp_cost_m
         const Bounds b = grid_search(C, p, cfg, sim_eval, &u, &r);
         std::memcpy(out, b.data(), b.size() * sizeof(int64_t));
         *ttft = r.ttft;
+    });
+}
+
+kvp_status kvp_simulate_ttft_causal(int32_t strategy, int64_t C, const int64_t* b, int64_t p, int64_t L,
+                                    const kvp_cost_model* cost, const kvp_network_model* net, double* out) {
+    return guard([&] {
+        Noise nz;
+        nz.causal = true;
+        *out = simulate(strategy, C, b, p, L, *cost, *net, nz);
+    });
+}
+
+kvp_status kvp_search_partition_causal(int64_t C, int64_t p, int64_t L, const kvp_cost_model* cost,
+                                       const kvp_network_model* net, const kvp_search_config* cfg, int64_t* out,
+                                       kvp_search_result* res) {
+    return guard([&] {
+        Noise nz;
+        nz.causal = true;
+        if (p == 1) {
+            const Bounds b = even_split(C, 1);
+            std::memcpy(out, b.data(), b.size() * sizeof(int64_t));
+            res->ttft = simulate(KVP_SERIAL, C, b.data(), 1, L, *cost, *net, nz);
+            res->evaluations = 1;
+            res->levels = 0;
+            return;
+        }
+        SimUser u{L, *cost, *net, true};
+        const Bounds b = grid_search(C, p, *cfg, sim_eval, &u, res);
+        std::memcpy(out, b.data(), b.size() * sizeof(int64_t));
     });
 }
 

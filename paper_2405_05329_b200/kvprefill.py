@@ -142,6 +142,10 @@ _SIGS = {
                                        C.POINTER(_SearchCfg), _I64P, C.POINTER(_SearchRes)]),
     "kvp_practical_bound": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.POINTER(_Cost), _I64P,
                                       C.POINTER(C.c_double)]),
+    "kvp_simulate_ttft_causal": (C.c_int, [C.c_int32, C.c_int64, _I64P, C.c_int64, C.c_int64, C.POINTER(_Cost),
+                                           C.POINTER(_Net), C.POINTER(C.c_double)]),
+    "kvp_search_partition_causal": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.POINTER(_Cost), C.POINTER(_Net),
+                                              C.POINTER(_SearchCfg), _I64P, C.POINTER(_SearchRes)]),
     "kvp_simulate_ttft_noisy": (C.c_int, [C.c_int32, C.c_int64, _I64P, C.c_int64, C.c_int64, C.POINTER(_Cost),
                                           C.POINTER(_Net), C.c_uint64, C.c_double, C.POINTER(C.c_double)]),
     "kvp_noise_study": (C.c_int, [C.c_int32, C.c_int64, _I64P, C.c_int64, C.c_int64, C.POINTER(_Cost),
@@ -627,6 +631,29 @@ def search_partition(C_: int, p: int, model: ModelConfig, cost: CostModel, net: 
     return SearchResult(ContextPartition(C_, out.tolist()), res.ttft, res.evaluations, res.levels)
 
 
+def simulate_ttft_causal(strategy: Strategy, partition: ContextPartition, model: ModelConfig, cost: CostModel,
+                         net: NetworkModel) -> float:
+    """Extension: simulate_ttft with attention priced on causal-visible pairs (B200 kernels)."""
+    b = _i64(partition.boundaries)
+    out = C.c_double()
+    cc, nc = cost._c(), net._c()
+    _check(lib().kvp_simulate_ttft_causal(int(strategy), partition.context_length, _ip(b), len(b) - 1,
+                                          model.n_layers, C.byref(cc), C.byref(nc), C.byref(out)),
+           "simulate_ttft_causal")
+    return out.value
+
+
+def search_partition_causal(C_: int, p: int, model: ModelConfig, cost: CostModel, net: NetworkModel,
+                            config: Optional[SearchConfig] = None) -> SearchResult:
+    config = config or SearchConfig()
+    out = np.zeros(p + 1, np.int64)
+    res = _SearchRes()
+    cc, nc, sc = cost._c(), net._c(), config._c()
+    _check(lib().kvp_search_partition_causal(C_, p, model.n_layers, C.byref(cc), C.byref(nc), C.byref(sc),
+                                             _ip(out), C.byref(res)), "search_partition_causal")
+    return SearchResult(ContextPartition(C_, out.tolist()), res.ttft, res.evaluations, res.levels)
+
+
 def ttft_star(C_: int, p: int, alpha: float) -> float:
     out = C.c_double()
     _check(lib().kvp_ttft_star(C_, p, alpha, C.byref(out)), "ttft_star")
@@ -660,142 +687,43 @@ def fit_cost_model(local_rows, held_rows, proj_s, rest_s) -> CostModel:
     return CostModel(out.alpha, out.proj_coeff, out.softmax_coeff, out.fixed_overhead)
 
 
-def calibrate_cost_model(weights: WeightSet, C_: int, p: int, reps: int = 3) -> CostModel:
-    """Fits the balancer's CostModel to MEASURED B200 layer times: one rank's layer executor is
-    timed in isolation on a grid of (local rows, prefix) points that spans the partitions
-    the search will visit at (C, p), then kvp_fit_cost_model solves proj ~ a*c and
-    rest ~ alpha*c*held + s*c + f.  Times are per layer; simulate_ttft multiplies by L."""
-    rows, held, proj, rest = [], [], [], []
+def profile_grid(weights: WeightSet, C_: int, p: int, reps: int = 3):
+    """Measured per-rank layer times on a grid of (local rows c, prefix b) points spanning the
+    partitions a search at (C, p) visits: list of (c, b, proj_s, rest_s)."""
+    pts = []
     for frac in (0.5, 1.0, 1.5):
         c = max(1, int(round(frac * C_ / p)))
         for b in sorted({0, C_ // 4, C_ // 2, (3 * C_) // 4}):
             if b + c > C_:
                 continue
             pm, rm = weights.profile_layer(c, b, reps)
-            rows.append(c)
-            held.append(b + c)
-            proj.append(pm * 1e-3)
-            rest.append(rm * 1e-3)
-    return fit_cost_model(rows, held, proj, rest)
+            pts.append((c, b, pm * 1e-3, rm * 1e-3))
+    return pts
 
 
-@dataclass
-class NoiseSidecar:
-    """simnet.hpp:65-78: per layer one adjacent link (drawn from (seed, layer)) runs at
-    bandwidth / slowdown_factor."""
-    seed: int = 1
-    slowdown_factor: float = 1.0
+def fit_causal_cost_model(points) -> CostModel:
+    """Extension: CostModel whose alpha prices causal-visible pairs c*(b + (c+1)/2) -- the work
+    of the tile-skipping B200 attention -- for simulate_ttft_causal / search_partition_causal."""
+    c = np.array([x[0] for x in points], np.float64)
+    b = np.array([x[1] for x in points], np.float64)
+    proj = np.array([x[2] for x in points], np.float64)
+    rest = np.array([x[3] for x in points], np.float64)
+    a = float(np.dot(proj, c) / np.dot(c, c))
+    X = np.stack([c * (b + 0.5 * (c + 1)), c, np.ones_like(c)], 1)
+    w, *_ = np.linalg.lstsq(X, rest, rcond=None)
+    w = np.maximum(w, 0.0)
+    return CostModel(alpha=float(max(w[0], 1e-300)), proj_coeff=a, softmax_coeff=float(w[1]),
+                     fixed_overhead=float(w[2]))
 
 
-def simulate_ttft_noisy(strategy: Strategy, partition: ContextPartition, model: ModelConfig, cost: CostModel,
-                        net: NetworkModel, noise: NoiseSidecar) -> float:
-    b = _i64(partition.boundaries)
-    out = C.c_double()
-    cc, nc = cost._c(), net._c()
-    _check(lib().kvp_simulate_ttft_noisy(int(strategy), partition.context_length, _ip(b), len(b) - 1,
-                                         model.n_layers, C.byref(cc), C.byref(nc), noise.seed, noise.slowdown_factor,
-                                         C.byref(out)), "simulate_ttft_noisy")
-    return out.value
-
-
-@dataclass
-class NoiseStudy:
-    quiet_ttft: float
-    mean_degradation: float
-    max_degradation: float
-    per_trial: list
-
-
-def noise_study(strategy: Strategy, partition: ContextPartition, model: ModelConfig, cost: CostModel,
-                net: NetworkModel, slowdown_factor: float, trials: int, seed: int) -> NoiseStudy:
-    """noise_study (simnet.hpp:332-353)."""
-    b = _i64(partition.boundaries)
-    q, mean, mx = C.c_double(), C.c_double(), C.c_double()
-    per = np.zeros(max(trials, 1), np.float64)
-    cc, nc = cost._c(), net._c()
-    _check(lib().kvp_noise_study(int(strategy), partition.context_length, _ip(b), len(b) - 1, model.n_layers,
-                                 C.byref(cc), C.byref(nc), slowdown_factor, trials, seed, C.byref(q), C.byref(mean),
-                                 C.byref(mx), _vp(per)), "noise_study")
-    return NoiseStudy(q.value, mean.value, mx.value, per[:trials].tolist())
-
-
-@dataclass
-class PartitionLookupTable:
-    """KVR-P table (lookup_table.hpp:22-39): context length -> ratios, JSON schema
-    {"p": int, "entries": [{"context_length": int, "ratios": [float]}]} (lookup_table.hpp:72-97)."""
-    process_count: int = 0
-    entries: dict = field(default_factory=dict)
-
-    def insert(self, context_length: int, ratios) -> None:
-        if self.process_count < 1:
-            raise LookupError_("table process count not set")
-        if len(ratios) != self.process_count:
-            raise LookupError_("ratio vector arity must equal the table process count")
-        if any(r < 0 for r in ratios):
-            raise LookupError_("table ratios must be non-negative")
-        if abs(sum(ratios) - 1.0) > 1e-9:
-            raise LookupError_("table ratios must sum to 1")
-        if context_length < 1:
-            raise LookupError_("context length must be positive")
-        self.entries[int(context_length)] = [float(r) for r in ratios]
-
-    def _arrays(self):
-        keys = sorted(self.entries)
-        Cs = np.asarray(keys, np.int64)
-        R = np.ascontiguousarray([self.entries[k] for k in keys], dtype=np.float64).reshape(len(keys), -1) \
-            if keys else np.zeros((0, max(self.process_count, 1)))
-        return Cs, R
-
-    def to_json(self) -> dict:
-        return {"p": self.process_count,
-                "entries": [{"context_length": k, "ratios": self.entries[k]} for k in sorted(self.entries)]}
-
-    @staticmethod
-    def from_json(doc: dict) -> "PartitionLookupTable":
-        try:
-            t = PartitionLookupTable(int(doc["p"]))
-            for e in doc["entries"]:
-                t.insert(int(e["context_length"]), list(e["ratios"]))
-        except (KeyError, TypeError, ValueError) as ex:
-            raise LookupError_(f"malformed lookup table: {ex}")
-        return t
-
-    def save(self, path: str) -> None:
-        import json
-        try:
-            with open(path, "w") as f:
-                json.dump(self.to_json(), f, indent=2)
-                f.write("\n")
-        except OSError as ex:
-            raise IoError(f"cannot open table file for writing: {path}: {ex}")
-
-    @staticmethod
-    def load(path: str) -> "PartitionLookupTable":
-        import json
-        try:
-            with open(path) as f:
-                doc = json.load(f)
-        except OSError as ex:
-            raise IoError(f"cannot open table file: {path}: {ex}")
-        except ValueError as ex:
-            raise LookupError_(f"malformed lookup table JSON in {path}: {ex}")
-        return PartitionLookupTable.from_json(doc)
-
-
-def interpolate_partition(table: PartitionLookupTable, C_: int) -> list:
-    Cs, R = table._arrays()
-    p = max(table.process_count, 0)
-    out = np.zeros(max(p, 1), np.float64)
-    _check(lib().kvp_interpolate_partition(_ip(Cs), _vp(R), len(Cs), p, C_, _vp(out)), "interpolate_partition")
-    return out[:p].tolist()
-
-
-def partition_from_table(table: PartitionLookupTable, C_: int) -> ContextPartition:
-    Cs, R = table._arrays()
-    p = max(table.process_count, 0)
-    out = np.zeros(max(p, 1) + 1, np.int64)
-    _check(lib().kvp_partition_from_table(_ip(Cs), _vp(R), len(Cs), p, C_, _ip(out)), "partition_from_table")
-    return ContextPartition(C_, out[:p + 1].tolist())
+def calibrate_cost_model(weights: WeightSet, C_: int, p: int, reps: int = 3, points=None) -> CostModel:
+    """Fits the balancer's CostModel to MEASURED B200 layer times: one rank's layer executor is
+    timed in isolation on a grid of (local rows, prefix) points that spans the partitions
+    the search will visit at (C, p), then kvp_fit_cost_model solves proj ~ a*c and
+    rest ~ alpha*c*held + s*c + f.  Times are per layer; simulate_ttft multiplies by L."""
+    pts = points if points is not None else profile_grid(weights, C_, p, reps)
+    return fit_cost_model([x[0] for x in pts], [x[0] + x[1] for x in pts], [x[2] for x in pts],
+                          [x[3] for x in pts])
 
 
 def max_rel_dev(a, b) -> float:
