@@ -726,6 +726,125 @@ def calibrate_cost_model(weights: WeightSet, C_: int, p: int, reps: int = 3, poi
                           [x[3] for x in pts])
 
 
+@dataclass
+class NoiseSidecar:
+    """simnet.hpp:65-78: per layer one adjacent link (drawn from (seed, layer)) runs at
+    bandwidth / slowdown_factor."""
+    seed: int = 1
+    slowdown_factor: float = 1.0
+
+
+def simulate_ttft_noisy(strategy: Strategy, partition: ContextPartition, model: ModelConfig, cost: CostModel,
+                        net: NetworkModel, noise: NoiseSidecar) -> float:
+    b = _i64(partition.boundaries)
+    out = C.c_double()
+    cc, nc = cost._c(), net._c()
+    _check(lib().kvp_simulate_ttft_noisy(int(strategy), partition.context_length, _ip(b), len(b) - 1,
+                                         model.n_layers, C.byref(cc), C.byref(nc), noise.seed, noise.slowdown_factor,
+                                         C.byref(out)), "simulate_ttft_noisy")
+    return out.value
+
+
+@dataclass
+class NoiseStudy:
+    quiet_ttft: float
+    mean_degradation: float
+    max_degradation: float
+    per_trial: list
+
+
+def noise_study(strategy: Strategy, partition: ContextPartition, model: ModelConfig, cost: CostModel,
+                net: NetworkModel, slowdown_factor: float, trials: int, seed: int) -> NoiseStudy:
+    """noise_study (simnet.hpp:332-353)."""
+    b = _i64(partition.boundaries)
+    q, mean, mx = C.c_double(), C.c_double(), C.c_double()
+    per = np.zeros(max(trials, 1), np.float64)
+    cc, nc = cost._c(), net._c()
+    _check(lib().kvp_noise_study(int(strategy), partition.context_length, _ip(b), len(b) - 1, model.n_layers,
+                                 C.byref(cc), C.byref(nc), slowdown_factor, trials, seed, C.byref(q), C.byref(mean),
+                                 C.byref(mx), _vp(per)), "noise_study")
+    return NoiseStudy(q.value, mean.value, mx.value, per[:trials].tolist())
+
+
+@dataclass
+class PartitionLookupTable:
+    """KVR-P table (lookup_table.hpp:22-39): context length -> ratios, JSON schema
+    {"p": int, "entries": [{"context_length": int, "ratios": [float]}]} (lookup_table.hpp:72-97)."""
+    process_count: int = 0
+    entries: dict = field(default_factory=dict)
+
+    def insert(self, context_length: int, ratios) -> None:
+        if self.process_count < 1:
+            raise LookupError_("table process count not set")
+        if len(ratios) != self.process_count:
+            raise LookupError_("ratio vector arity must equal the table process count")
+        if any(r < 0 for r in ratios):
+            raise LookupError_("table ratios must be non-negative")
+        if abs(sum(ratios) - 1.0) > 1e-9:
+            raise LookupError_("table ratios must sum to 1")
+        if context_length < 1:
+            raise LookupError_("context length must be positive")
+        self.entries[int(context_length)] = [float(r) for r in ratios]
+
+    def _arrays(self):
+        keys = sorted(self.entries)
+        Cs = np.asarray(keys, np.int64)
+        R = np.ascontiguousarray([self.entries[k] for k in keys], dtype=np.float64).reshape(len(keys), -1) \
+            if keys else np.zeros((0, max(self.process_count, 1)))
+        return Cs, R
+
+    def to_json(self) -> dict:
+        return {"p": self.process_count,
+                "entries": [{"context_length": k, "ratios": self.entries[k]} for k in sorted(self.entries)]}
+
+    @staticmethod
+    def from_json(doc: dict) -> "PartitionLookupTable":
+        try:
+            t = PartitionLookupTable(int(doc["p"]))
+            for e in doc["entries"]:
+                t.insert(int(e["context_length"]), list(e["ratios"]))
+        except (KeyError, TypeError, ValueError) as ex:
+            raise LookupError_(f"malformed lookup table: {ex}")
+        return t
+
+    def save(self, path: str) -> None:
+        import json
+        try:
+            with open(path, "w") as f:
+                json.dump(self.to_json(), f, indent=2)
+                f.write("\n")
+        except OSError as ex:
+            raise IoError(f"cannot open table file for writing: {path}: {ex}")
+
+    @staticmethod
+    def load(path: str) -> "PartitionLookupTable":
+        import json
+        try:
+            with open(path) as f:
+                doc = json.load(f)
+        except OSError as ex:
+            raise IoError(f"cannot open table file: {path}: {ex}")
+        except ValueError as ex:
+            raise LookupError_(f"malformed lookup table JSON in {path}: {ex}")
+        return PartitionLookupTable.from_json(doc)
+
+
+def interpolate_partition(table: PartitionLookupTable, C_: int) -> list:
+    Cs, R = table._arrays()
+    p = max(table.process_count, 0)
+    out = np.zeros(max(p, 1), np.float64)
+    _check(lib().kvp_interpolate_partition(_ip(Cs), _vp(R), len(Cs), p, C_, _vp(out)), "interpolate_partition")
+    return out[:p].tolist()
+
+
+def partition_from_table(table: PartitionLookupTable, C_: int) -> ContextPartition:
+    Cs, R = table._arrays()
+    p = max(table.process_count, 0)
+    out = np.zeros(max(p, 1) + 1, np.int64)
+    _check(lib().kvp_partition_from_table(_ip(Cs), _vp(R), len(Cs), p, C_, _ip(out)), "partition_from_table")
+    return ContextPartition(C_, out[:p + 1].tolist())
+
+
 def max_rel_dev(a, b) -> float:
     """max_rel_dev (matrix.hpp:101-115): max |a - b| / max(1, |b|)."""
     a = np.asarray(a, np.float64)

@@ -263,3 +263,23 @@ def test_noise_and_table_bit_exact_vs_reference():
         r_ref, b_ref = ref.table(entries, p, q)
         assert kv.interpolate_partition(t, q) == r_ref
         assert kv.partition_from_table(t, q).boundaries == b_ref
+
+
+def test_causal_cost_model_extension():
+    """Extension (not in the reference): attention priced on causal-visible pairs."""
+    m = kv.ModelConfig(64, 4, 4, 2, 1, "f32", True)
+    cost = kv.CostModel(alpha=1e-6, proj_coeff=0.0, softmax_coeff=0.0, fixed_overhead=0.0)
+    net = kv.NetworkModel(bandwidth=1e30, latency=0.0)
+    one = kv.even_partition(1000, 1)
+    dense = kv.simulate_ttft(kv.Strategy.KVR, one, m, cost, net)
+    causal = kv.simulate_ttft_causal(kv.Strategy.KVR, one, m, cost, net)
+    assert abs(dense - 2 * 1e-6 * 1000 * 1000) < 1e-12
+    assert abs(causal - 2 * 1e-6 * 1000 * 500.5) < 1e-12
+    even = kv.even_partition(8192, 4)
+    for s in (kv.Strategy.KVR, kv.Strategy.TSP):
+        assert kv.simulate_ttft_causal(s, even, m, cost, net) < kv.simulate_ttft(s, even, m, cost, net)
+    found = kv.search_partition_causal(8192, 4, m, cost, net)
+    sizes = found.partition.sizes()
+    assert sum(sizes) == 8192
+    assert all(sizes[i] >= sizes[i + 1] for i in range(3))
+    assert found.ttft <= kv.simulate_ttft_causal(kv.Strategy.KVR, even, m, cost, net)
