@@ -81,6 +81,8 @@ struct Cfg {
     static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr uint32_t TMEM_COLS = 2 * BN;
     static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr uint32_t STAGING = EPI_WARPS * 32 * 32 * 4;  // EPI_RESID transpose tiles
+    static constexpr uint32_t smem_for(int kind) { return SMEM + (kind == EPI_RESID ? STAGING : 0); }
 };
 
 struct EpiArgs {
@@ -102,54 +104,12 @@ struct EpiArgs {
     float inv_norm_cols;
 };
 
-// Returns the sum of squares of the stored values (EPI_RESID; feeds the fused RMSNorm).
+// QKV split / ReLU / plain bf16 store of one 32-column chunk (lane = row).
 template <int KIND>
-__device__ __forceinline__ float store_chunk(const EpiArgs& ep, int64_t row, int64_t col0, int64_t N,
-                                             const uint32_t (&r)[32], float row_scale) {
+__device__ __forceinline__ void store_chunk(const EpiArgs& ep, int64_t row, int64_t col0, int64_t N,
+                                            const uint32_t (&r)[32], float row_scale) {
     const bool full = col0 + 32 <= N;
-    float ss = 0.f;
-    if constexpr (KIND == EPI_RESID) {
-        float* o = ep.outf + row * ep.ldf + col0;
-        const float* rs = ep.resid + row * ep.ldr + col0;
-        bf16* ob = ep.outb ? ep.outb + row * ep.ldb + col0 : nullptr;
-        if (full) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-                const float4 a = *reinterpret_cast<const float4*>(rs + j);
-                const float4 b = *reinterpret_cast<const float4*>(rs + j + 4);
-                float4 v, w;
-                v.x = a.x + __uint_as_float(r[j + 0]);
-                v.y = a.y + __uint_as_float(r[j + 1]);
-                v.z = a.z + __uint_as_float(r[j + 2]);
-                v.w = a.w + __uint_as_float(r[j + 3]);
-                w.x = b.x + __uint_as_float(r[j + 4]);
-                w.y = b.y + __uint_as_float(r[j + 5]);
-                w.z = b.z + __uint_as_float(r[j + 6]);
-                w.w = b.w + __uint_as_float(r[j + 7]);
-                *reinterpret_cast<float4*>(o + j) = v;
-                *reinterpret_cast<float4*>(o + j + 4) = w;
-                ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w + w.x * w.x + w.y * w.y + w.z * w.z + w.w * w.w;
-                if (ob) {
-                    uint4 pk;
-                    pk.x = ptx::pack_bf16(v.x, v.y);
-                    pk.y = ptx::pack_bf16(v.z, v.w);
-                    pk.z = ptx::pack_bf16(w.x, w.y);
-                    pk.w = ptx::pack_bf16(w.z, w.w);
-                    *reinterpret_cast<uint4*>(ob + j) = pk;
-                }
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                if (col0 + j < N) {
-                    const float v = rs[j] + __uint_as_float(r[j]);
-                    o[j] = v;
-                    ss += v * v;
-                    if (ob) ob[j] = __float2bfloat16_rn(v);
-                }
-            }
-        }
-    } else {
+    {
         bf16* o;
         if constexpr (KIND == EPI_QKV) {
             // chunks straddling the Q|K|V column boundaries (q or kv not a multiple of 32)
@@ -164,7 +124,7 @@ __device__ __forceinline__ float store_chunk(const EpiArgs& ep, int64_t row, int
                                        : (c < e1 ? ep.out1 + row * ep.ld1 + (c - e0) : ep.out2 + row * ep.ld2 + (c - e1));
                     *dst = __float2bfloat16_rn(__uint_as_float(r[j]) * row_scale);
                 }
-                return 0.f;
+                return;
             }
             if (col0 < ep.n0) {
                 o = ep.out0 + row * ep.ld0 + col0;
@@ -198,33 +158,117 @@ __device__ __forceinline__ float store_chunk(const EpiArgs& ep, int64_t row, int
                 if (col0 + j < N) o[j] = __float2bfloat16_rn(v[j]);
         }
     }
-    return ss;
 }
 
-// EPI_RESID with the residual already in registers (prefetched before the accumulator was
-// ready): out = resid + acc (f32), bf16 copy, sum of squares.
-__device__ __forceinline__ float store_resid_prefetched(const EpiArgs& ep, int64_t row, int64_t col0,
-                                                        const uint32_t (&r)[32], const float4 (&rv)[8]) {
-    float* o = ep.outf + row * ep.ldf + col0;
-    bf16* ob = ep.outb ? ep.outb + row * ep.ldb + col0 : nullptr;
-    float ss = 0.f;
+// EPI_RESID epilogue, one 32x32 chunk per warp, coalesced: the accumulator (lane = row, from
+// tcgen05.ld 32x32b) is transposed through a 4 KB XOR-swizzled smem tile so that lane l then
+// owns rows {l/8 + 4i : i < 8} x columns [4*(l%8), 4*(l%8)+4) -- every global access of the
+// warp covers 4 full 128-byte row segments instead of 32 scattered 16-byte pieces.
+struct ResidT {
+    int64_t row0;  // first row of the warp's 32-row slab
+    uint32_t rsub, cg;
+};
+
+__device__ __forceinline__ void resid_fetch(const EpiArgs& ep, const ResidT& t, int64_t col0, int M, int N,
+                                            float4 (&rv)[8]) {
+    const bool full = t.row0 + 32 <= M && col0 + 32 <= N;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        float4 v;
-        v.x = rv[j].x + __uint_as_float(r[4 * j + 0]);
-        v.y = rv[j].y + __uint_as_float(r[4 * j + 1]);
-        v.z = rv[j].z + __uint_as_float(r[4 * j + 2]);
-        v.w = rv[j].w + __uint_as_float(r[4 * j + 3]);
-        *reinterpret_cast<float4*>(o + 4 * j) = v;
-        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
-        if (ob) {
-            uint2 pk;
-            pk.x = ptx::pack_bf16(v.x, v.y);
-            pk.y = ptx::pack_bf16(v.z, v.w);
-            *reinterpret_cast<uint2*>(ob + 4 * j) = pk;
+    for (int i = 0; i < 8; ++i) {
+        const int64_t row = t.row0 + t.rsub + 4 * i;
+        const int64_t col = col0 + 4 * t.cg;
+        if (full) {
+            rv[i] = *reinterpret_cast<const float4*>(ep.resid + row * ep.ldr + col);
+        } else {
+            float e[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (row < M && col + q < N) e[q] = ep.resid[row * ep.ldr + col + q];
+            rv[i] = make_float4(e[0], e[1], e[2], e[3]);
         }
     }
-    return ss;
+}
+
+__device__ __forceinline__ float sq4(float4 v) {
+    return __fmaf_rn(v.w, v.w, __fmaf_rn(v.z, v.z, __fmaf_rn(v.y, v.y, __fmul_rn(v.x, v.x))));
+}
+
+// Adds the chunk to the prefetched residual, stores f32 + bf16, accumulates per-row partial
+// sums of squares in ss[i] (row rsub + 4i).
+__device__ __forceinline__ void resid_store(const EpiArgs& ep, const ResidT& t, int64_t col0, int M, int N,
+                                            const uint32_t (&r)[32], const float4 (&rv)[8], float* stg,
+                                            float (&ss)[8]) {
+    const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+        *reinterpret_cast<float4*>(stg + lane * 32 + ((g ^ (lane & 7)) << 2)) =
+            make_float4(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1]), __uint_as_float(r[4 * g + 2]),
+                        __uint_as_float(r[4 * g + 3]));
+    __syncwarp();
+    const bool full = t.row0 + 32 <= M && col0 + 32 <= N;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t rr = t.rsub + 4 * i;
+        const float4 a = *reinterpret_cast<const float4*>(stg + rr * 32 + ((t.cg ^ (rr & 7)) << 2));
+        float4 v;
+        v.x = rv[i].x + a.x;
+        v.y = rv[i].y + a.y;
+        v.z = rv[i].z + a.z;
+        v.w = rv[i].w + a.w;
+        const int64_t row = t.row0 + rr, col = col0 + 4 * t.cg;
+        if (full) {
+            *reinterpret_cast<float4*>(ep.outf + row * ep.ldf + col) = v;
+            if (ep.outb) {
+                uint2 pk;
+                pk.x = ptx::pack_bf16(v.x, v.y);
+                pk.y = ptx::pack_bf16(v.z, v.w);
+                *reinterpret_cast<uint2*>(ep.outb + row * ep.ldb + col) = pk;
+            }
+            ss[i] = __fadd_rn(ss[i], sq4(v));
+        } else if (row < M) {
+            float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (col + q < N) {
+                    ep.outf[row * ep.ldf + col + q] = e[q];
+                    if (ep.outb) ep.outb[row * ep.ldb + col + q] = __float2bfloat16_rn(e[q]);
+                } else {
+                    e[q] = 0.f;
+                }
+            }
+            // same rounding sequence as the full path: a row's partial never depends on
+            // whether its 32-row slab is complete (partition-independent results)
+            ss[i] = __fadd_rn(ss[i], sq4(make_float4(e[0], e[1], e[2], e[3])));
+        }
+    }
+    __syncwarp();  // the tile is rewritten by the next chunk
+}
+
+// Reduce-scatter of ss[0..7] over the 8 lanes sharing rsub (7 shuffles): afterwards lane cg
+// holds the total for row rsub + 4*cg; written as the row's partial of 64-column group grp.
+__device__ __forceinline__ void resid_ssq_flush(const EpiArgs& ep, const ResidT& t, int M, int64_t grp,
+                                                float (&ss)[8]) {
+    float a4[4], a2[2], a1;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const bool hi = t.cg & 4;
+        const float send = hi ? ss[j] : ss[j + 4];
+        a4[j] = (hi ? ss[j + 4] : ss[j]) + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const bool hi = t.cg & 2;
+        const float send = hi ? a4[j] : a4[j + 2];
+        a2[j] = (hi ? a4[j + 2] : a4[j]) + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+    {
+        const bool hi = t.cg & 1;
+        const float send = hi ? a2[0] : a2[1];
+        a1 = (hi ? a2[1] : a2[0]) + __shfl_xor_sync(0xffffffffu, send, 1);
+    }
+    const int64_t row = t.row0 + t.rsub + 4 * t.cg;
+    if (row < M) ep.ssq_out[row * ep.ssq_parts + grp] = a1;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ss[i] = 0.f;
 }
 
 template <int BN, int KIND>
@@ -352,21 +396,18 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + buf * BN;
             float ssacc = 0.f;
             if constexpr (KIND == EPI_RESID) {
-                // The residual does not depend on the accumulator: fetch two chunks of it while
-                // the tile's MMAs are still running, then keep two chunks in flight.
+                // The residual does not depend on the accumulator: fetch the first chunk of it
+                // while the tile's MMAs are still running, then one chunk ahead.
+                const ResidT rt{static_cast<int64_t>(m_blk) * BM + quarter * 32, lane >> 3, lane & 7};
+                float* stg = reinterpret_cast<float*>(smem + STAGES * C::STAGE_BYTES + 256) + (warp - 2) * 1024;
                 float4 rv[8];
-                auto fetch = [&](int cc) {
-                    const int64_t col0 = static_cast<int64_t>(col_base) + (half * MY + cc) * 32;
-                    if (row < M && col0 + 32 <= N) {
-                        const float4* src = reinterpret_cast<const float4*>(ep.resid + row * ep.ldr + col0);
+                float ss[8];
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) rv[j] = src[j];
-                    }
-                };
-                fetch(0);
+                for (int i = 0; i < 8; ++i) ss[i] = 0.f;
+                resid_fetch(ep, rt, static_cast<int64_t>(col_base) + half * MY * 32, M, N, rv);
                 ptx::mbar_wait(&tfull[buf], aphase);
                 ptx::tc_fence_after();
-#pragma unroll
+#pragma unroll 1
                 for (int cc = 0; cc < MY_MAX; ++cc) {
                     if (cc >= MY) break;
                     const int c = half * MY + cc;
@@ -375,18 +416,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                     uint32_t r[32];
                     ptx::tmem_ld32(taddr + c * 32, r);
                     ptx::tmem_ld_wait();
-                    if (row < M) {
-                        if (col0 + 32 <= N)
-                            ssacc += store_resid_prefetched(ep, row, col0, r, rv);
-                        else
-                            ssacc += store_chunk<KIND>(ep, row, col0, N, r, 1.f);
-                    }
-                    if (cc + 1 < MY) fetch(cc + 1);
+                    resid_store(ep, rt, col0, M, N, r, rv, stg, ss);
+                    if (cc + 1 < MY && col0 + 32 < N) resid_fetch(ep, rt, col0 + 32, M, N, rv);
                     // one partial per 64-column group, independent of BN and of the warp split
-                    if (ep.ssq_out != nullptr && row < M && (((c + 1) & 1) == 0 || col0 + 32 >= N)) {
-                        ep.ssq_out[row * ep.ssq_parts + (col0 >> 6)] = ssacc;
-                        ssacc = 0.f;
-                    }
+                    if (ep.ssq_out != nullptr && (((c + 1) & 1) == 0 || col0 + 32 >= N))
+                        resid_ssq_flush(ep, rt, M, col0 >> 6, ss);
                 }
             } else {
                 ptx::mbar_wait(&tfull[buf], aphase);
@@ -430,7 +464,7 @@ void launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& 
     int dev = 0;
     cudaGetDevice(&dev);
     if (configured_dev != dev) {  // attribute is per device; cheap to re-set
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::smem_for(KIND));
         configured_dev = dev;
     }
     const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
@@ -444,7 +478,7 @@ void launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& 
     const int rem = tiles % grid;
     const int n_full = (split_tail && BN == 256 && tiles > grid && rem > 0 && 2 * rem <= grid) ? tiles - rem : tiles;
     note_launch();
-    kern<<<grid, THREADS, Cfg<BN>::SMEM, s>>>(ta, tb, tbh, M, N, K, n_full, ep);
+    kern<<<grid, THREADS, Cfg<BN>::smem_for(KIND), s>>>(ta, tb, tbh, M, N, K, n_full, ep);
 }
 
 template <int BN>
