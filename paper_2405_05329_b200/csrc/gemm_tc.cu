@@ -274,7 +274,8 @@ __device__ __forceinline__ void resid_ssq_flush(const EpiArgs& ep, const ResidT&
 template <int BN, int KIND>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmBh, int M, int N, int K, int n_full, EpiArgs ep) {
+                   const __grid_constant__ CUtensorMap tmBh, int M, int N, int K, int n_full, int group_m,
+                   EpiArgs ep) {
     using C = Cfg<BN>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -292,15 +293,27 @@ __global__ void __launch_bounds__(THREADS, 1)
     // BN/2-wide tiles each so the persistent grid's final round is evenly filled.  Only the
     // tile width changes, not the per-element K order: results are identical either way.
     const int num_tiles = n_full + 2 * (num_m * num_n - n_full);
+    // Grouped rasterisation: tiles run in groups of `group_m` M-blocks, M-fastest inside a
+    // group, so the CTAs in flight share a group_m x ~(148/group_m) block of the output: the
+    // group's A rows (group_m*BM*K*2 bytes, sized on the host to stay in L2) are read from
+    // HBM once and each weight column block once per group.
+    auto coords = [&](int big, int& m_blk, int& n_blk) {
+        const int per_group = group_m * num_n;
+        const int grp = big / per_group, rem = big - grp * per_group;
+        const int g_m = min(group_m, num_m - grp * group_m);
+        m_blk = grp * group_m + rem % g_m;
+        n_blk = rem / g_m;
+    };
     auto decode = [&](int tile, int& m_blk, int& col_base, int& width) {
+        int n_blk;
         if (tile < n_full) {
-            m_blk = tile % num_m;
-            col_base = (tile / num_m) * BN;
+            coords(tile, m_blk, n_blk);
+            col_base = n_blk * BN;
             width = BN;
         } else {
-            const int k = tile - n_full, big = n_full + (k >> 1);
-            m_blk = big % num_m;
-            col_base = (big / num_m) * BN + (k & 1) * (BN / 2);
+            const int k = tile - n_full;
+            coords(n_full + (k >> 1), m_blk, n_blk);
+            col_base = n_blk * BN + (k & 1) * (BN / 2);
             width = BN / 2;
         }
     };
@@ -477,8 +490,17 @@ void launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& 
     }();
     const int rem = tiles % grid;
     const int n_full = (split_tail && BN == 256 && tiles > grid && rem > 0 && 2 * rem <= grid) ? tiles - rem : tiles;
+    // M-blocks per raster group: keep the group's A rows within ~32 MB of L2
+    static const int forced_group = [] {
+        const char* e = getenv("KVP_GEMM_GROUP");
+        return e ? atoi(e) : 0;
+    }();
+    const int num_m = (M + BM - 1) / BM;
+    int group_m = forced_group > 0 ? forced_group : static_cast<int>((32ll << 20) / (static_cast<int64_t>(BM) * K * 2));
+    group_m = group_m < 4 ? 4 : group_m;
+    group_m = group_m > num_m ? num_m : group_m;
     note_launch();
-    kern<<<grid, THREADS, Cfg<BN>::smem_for(KIND), s>>>(ta, tb, tbh, M, N, K, n_full, ep);
+    kern<<<grid, THREADS, Cfg<BN>::smem_for(KIND), s>>>(ta, tb, tbh, M, N, K, n_full, group_m, ep);
 }
 
 template <int BN>

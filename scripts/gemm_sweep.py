@@ -13,6 +13,8 @@ shapes = {  # name: (M, N, K, epi)
     "p8_qkv": (512, 12288, 4096, 0), "p8_o": (512, 4096, 4096, 1), "p8_ffn1": (512, 8192, 4096, 2),
     "p8_ffn2": (512, 4096, 8192, 1), "falcon_qkv": (8192, 4672, 4544, 0), "falcon_o": (8192, 4544, 4544, 1),
     "sq8192": (8192, 8192, 8192, 3),
+    "l16_qkv": (16384, 12288, 4096, 0), "l16_o": (16384, 4096, 4096, 1), "l16_ffn1": (16384, 8192, 4096, 2),
+    "l16_ffn2": (16384, 4096, 8192, 1),
 }
 only = set(sys.argv[1:])
 out = {}
