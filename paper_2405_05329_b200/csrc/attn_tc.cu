@@ -103,8 +103,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
     using C = ACfg<HD>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-B alignment by pointer arithmetic on the __shared__ array, so the compiler keeps
+    // the shared state space (LDS/STS instead of generic loads/stores)
+    uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
     uint8_t* sQ = smem;                  // [2] query tiles
     uint8_t* sK = sQ + 2 * C::Q_BYTES;   // [2] stages
     uint8_t* sV = sK + 2 * C::KV_BYTES;  // [2] stages

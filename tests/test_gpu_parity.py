@@ -274,3 +274,23 @@ def test_llama7b_shape_strategy_invariance_bf16():
     ref = O.forward_serial(m, O.init_weights(m, np.float32), ctx[:96])
     assert kv.max_rel_dev(one.first_token_hidden, ref[-1:]) <= BF16_TOL
     assert argmax_ok(one.first_token_hidden[0], ref[-1], BF16_TOL)
+
+
+@pytest.mark.parametrize("d,h,kvh", [(1024, 8, 8), (512, 8, 8), (4096, 32, 32)])
+def test_attention_split_invariance_bitwise(d, h, kvh):
+    """Rows of a causal attention computed inside any rank's slice (arbitrary, unaligned
+    offsets) equal the same rows of the single-rank computation bit for bit, and repeated
+    launches are deterministic -- the kernel property Serial == TSP == KVR rests on."""
+    W = engine(d, h, kvh, 1, 1, "bf16")
+    m = oracle_model(d, h, kvh, 1, 1)
+    C_ = 2048
+    for scale in (1.0, 4.0, 16.0):  # larger scores exercise the lazy O rescale
+        Q = O.random_context(C_, m.q_dim, 31, np.float32) * scale
+        K = O.random_context(C_, m.kv_dim, 32, np.float32) * scale
+        V = O.random_context(C_, m.kv_dim, 33, np.float32)
+        full = kv.causal_attention(Q, K, V, kv.CausalMask(0, C_), W)
+        for _ in range(2):
+            assert np.array_equal(full, kv.causal_attention(Q, K, V, kv.CausalMask(0, C_), W))
+        for lo, hi in ((819, 1433), (1433, 1843), (1843, 2048), (0, 819), (5, 300), (64, 192)):
+            part = kv.causal_attention(Q[lo:hi], K[:hi], V[:hi], kv.CausalMask(lo, hi - lo), W)
+            assert np.array_equal(part, full[lo:hi]), (scale, lo, hi, np.abs(part - full[lo:hi]).max())
