@@ -10,12 +10,15 @@
 //   * WeightSet<T> owns the device-resident weights + engine; init_weights<T>(cfg, devices)
 //     takes an optional device list (rank r runs on devices[r % n]);
 //   * KVR-S balancing from measured times: fit_cost_model + search_partition.
-// Out of scope here: commands.hpp, the CLI, lookup tables, noise studies.
+// The KVR-P lookup table and the noise study are here too (lookup_table.hpp, simnet.hpp);
+// their JSON file I/O is in table_io.hpp (needs nlohmann/json); the commands.hpp CLI is the
+// separate tool tools/kvprefill_b200_main.cpp.
 #pragma once
 
 #include <algorithm>
 #include <cmath>
 #include <limits>
+#include <map>
 #include <type_traits>
 #include <cstdint>
 #include <cstring>
@@ -426,12 +429,21 @@ Matrix<T> forward_serial_hidden(const Matrix<T>& context, const WeightSet<T>& we
 struct CostModel {
     double alpha = 1e-6, proj_coeff = 4e-6, softmax_coeff = 1e-7, fixed_overhead = 1e-5;
     kvp_cost_model c() const { return {alpha, proj_coeff, softmax_coeff, fixed_overhead}; }
+    void validate() const {  // simnet.hpp:32-36
+        if (!(alpha > 0)) throw ConfigError("cost.alpha must be positive");
+        if (proj_coeff < 0 || softmax_coeff < 0 || fixed_overhead < 0)
+            throw ConfigError("cost coefficients must be non-negative");
+    }
 };
 
 struct NetworkModel {
     double bandwidth = 1e7, latency = 1e-6;
     static NetworkModel zero_comm() { return {std::numeric_limits<double>::infinity(), 0.0}; }
     kvp_network_model c() const { return {bandwidth, latency}; }
+    void validate() const {  // simnet.hpp:51-54
+        if (!(bandwidth > 0)) throw ConfigError("network.bandwidth must be positive");
+        if (latency < 0) throw ConfigError("network.latency must be non-negative");
+    }
 };
 
 inline double simulate_ttft_value(Strategy s, const ContextPartition& part, const ModelConfig& model,
@@ -467,6 +479,101 @@ inline SearchResult search_partition(int64_t C, int64_t p, const ModelConfig& mo
     r.evaluations = res.evaluations;
     r.levels = res.levels;
     return r;
+}
+
+// practical_bound / ttft_practical_lower (simnet.hpp:297-321).
+struct PracticalBound {
+    ContextPartition partition;
+    double ttft = 0.0;
+};
+
+inline PracticalBound practical_bound(int64_t C, int64_t p, const ModelConfig& model, const CostModel& cost) {
+    PracticalBound b;
+    b.partition.context_length = C;
+    b.partition.boundaries.assign(static_cast<size_t>(std::max<int64_t>(p, 1) + 1), 0);
+    const kvp_cost_model cc = cost.c();
+    detail::check(kvp_practical_bound(C, p, model.n_layers, &cc, b.partition.boundaries.data(), &b.ttft),
+                  "practical_bound");
+    return b;
+}
+
+inline double ttft_practical_lower(int64_t C, int64_t p, const ModelConfig& model, const CostModel& cost) {
+    return practical_bound(C, p, model, cost).ttft;
+}
+
+// noise_study (simnet.hpp:323-353): seeded trials with one slowed link per layer.
+struct NoiseStudy {
+    double quiet_ttft = 0, mean_degradation = 0, max_degradation = 0;
+    std::vector<double> per_trial;
+};
+
+inline NoiseStudy noise_study(Strategy s, const ContextPartition& part, const ModelConfig& model,
+                              const CostModel& cost, const NetworkModel& net, double slowdown_factor,
+                              int64_t trials, uint64_t seed) {
+    NoiseStudy r;
+    r.per_trial.assign(static_cast<size_t>(std::max<int64_t>(trials, 1)), 0.0);
+    const kvp_cost_model cc = cost.c();
+    const kvp_network_model nc = net.c();
+    detail::check(kvp_noise_study(static_cast<int32_t>(s), part.context_length, part.boundaries.data(),
+                                  part.process_count(), model.n_layers, &cc, &nc, slowdown_factor, trials, seed,
+                                  &r.quiet_ttft, &r.mean_degradation, &r.max_degradation, r.per_trial.data()),
+                  "noise_study");
+    r.per_trial.resize(static_cast<size_t>(std::max<int64_t>(trials, 0)));
+    return r;
+}
+
+// KVR-P lookup table (lookup_table.hpp:22-70): context length -> per-rank ratios for one p.
+struct PartitionLookupTable {
+    int64_t process_count = 0;
+    std::map<int64_t, std::vector<double>> entries;
+
+    void insert(int64_t context_length, std::vector<double> ratios) {
+        if (process_count < 1) throw LookupError("table process count not set");
+        if (static_cast<int64_t>(ratios.size()) != process_count)
+            throw LookupError("ratio vector arity must equal the table process count");
+        double sum = 0;
+        for (double r : ratios) {
+            if (r < 0) throw LookupError("table ratios must be non-negative");
+            sum += r;
+        }
+        if (std::abs(sum - 1.0) > 1e-9) throw LookupError("table ratios must sum to 1");
+        if (context_length < 1) throw LookupError("context length must be positive");
+        entries[context_length] = std::move(ratios);
+    }
+};
+
+namespace detail {
+struct FlatTable {
+    std::vector<int64_t> keys;
+    std::vector<double> ratios;
+    explicit FlatTable(const PartitionLookupTable& t) {
+        for (const auto& [c, r] : t.entries) {
+            keys.push_back(c);
+            ratios.insert(ratios.end(), r.begin(), r.end());
+        }
+    }
+};
+}  // namespace detail
+
+inline std::vector<double> interpolate_partition(const PartitionLookupTable& table, int64_t C) {
+    const detail::FlatTable f(table);
+    std::vector<double> out(static_cast<size_t>(std::max<int64_t>(table.process_count, 1)));
+    detail::check(kvp_interpolate_partition(f.keys.data(), f.ratios.data(), static_cast<int64_t>(f.keys.size()),
+                                            table.process_count, C, out.data()),
+                  "interpolate_partition");
+    out.resize(static_cast<size_t>(std::max<int64_t>(table.process_count, 0)));
+    return out;
+}
+
+inline ContextPartition partition_from_table(const PartitionLookupTable& table, int64_t C) {
+    const detail::FlatTable f(table);
+    ContextPartition out;
+    out.context_length = C;
+    out.boundaries.assign(static_cast<size_t>(std::max<int64_t>(table.process_count, 1) + 1), 0);
+    detail::check(kvp_partition_from_table(f.keys.data(), f.ratios.data(), static_cast<int64_t>(f.keys.size()),
+                                           table.process_count, C, out.boundaries.data()),
+                  "partition_from_table");
+    return out;
 }
 
 }  // namespace kvprefill

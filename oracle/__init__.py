@@ -512,6 +512,13 @@ class Reference:
                   seed, C.byref(q), C.byref(mean), C.byref(mx), _ptr(per)), "ref noise_study")
         return q.value, mean.value, mx.value, per[:trials].tolist()
 
+    def cli(self, sub: str, config_path: str = "", C_: int = -1, out: str = "", table: str = "") -> int:
+        """The reference CLI's subcommand through its own commands.hpp (exit code)."""
+        fn = self.lib.kvref_cli
+        fn.restype = C.c_int
+        fn.argtypes = [C.c_char_p, C.c_char_p, C.c_int64, C.c_char_p, C.c_char_p]
+        return fn(sub.encode(), config_path.encode(), C_, out.encode(), table.encode())
+
     def table(self, entries: dict, p: int, C_: int):
         keys = list(entries)
         Cs = np.ascontiguousarray(keys, np.int64)

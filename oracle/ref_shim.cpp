@@ -9,7 +9,9 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <iostream>
 #include <memory>
+#include <string>
 
 #include "kvprefill/kvprefill.hpp"
 
@@ -314,4 +316,31 @@ int kvref_ttft_star(int64_t C, int64_t p, double alpha, double* out) { GUARD({ *
 
 double kvref_table_build_cost(double T, int64_t N, int64_t C) { return table_build_cost(T, N, C); }
 
+
+// The reference CLI's subcommands (commands.hpp cmd_*), config from a JSON file, with the
+// --out / --table overrides of tools/kvprefill_main.cpp; returns the CLI exit code
+// (ConfigError -> 2, other Error -> 1).
+int kvref_cli(const char* sub, const char* config_path, int64_t predict_c, const char* out_path,
+              const char* table_path) {
+    try {
+        ExperimentConfig cfg;
+        if (config_path && *config_path) cfg = load_experiment_config(config_path);
+        if (out_path && *out_path) cfg.out_path = out_path;
+        if (table_path && *table_path) cfg.table_path = table_path;
+        const std::string s(sub);
+        int rc = 2;
+        if (s == "verify") rc = cmd_verify(cfg);
+        else if (s == "sweep") rc = cmd_sweep(cfg);
+        else if (s == "search") rc = cmd_search(cfg);
+        else if (s == "predict") rc = cmd_predict(cfg, predict_c);
+        else if (s == "noise") rc = cmd_noise(cfg);
+        std::cout.flush();
+        std::cerr.flush();
+        return rc;
+    } catch (const ConfigError&) {
+        return 2;
+    } catch (const Error&) {
+        return 1;
+    }
+}
 }  // extern "C"

@@ -12,6 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libkvp_b200.so")
+CLI = os.path.join(OUT_DIR, "kvprefill_b200")
 ROOT = os.path.dirname(HERE)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -45,6 +46,32 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
+def _json_include() -> str:
+    """nlohmann/json (header-only, shipped in this image under cudnn_frontend)."""
+    import glob
+    cands = glob.glob(os.path.join(sys.prefix, "lib", "python3*", "site-packages", "include", "cudnn_frontend",
+                                   "thirdparty", "nlohmann", "json.hpp"))
+    if not cands:
+        raise RuntimeError("nlohmann/json.hpp not found (needed by the kvprefill_b200 CLI)")
+    return os.path.dirname(cands[0])
+
+
+def build_cli(verbose: bool = False) -> str:
+    """The reference-compatible CLI (tools/kvprefill_b200_main.cpp) over the C++ drop-in."""
+    src = os.path.join(ROOT, "tools", "kvprefill_b200_main.cpp")
+    hdrs = [os.path.join(ROOT, "include", "kvprefill_b200", h) for h in ("kvprefill.hpp", "table_io.hpp")]
+    if os.path.exists(CLI) and all(os.path.getmtime(f) <= os.path.getmtime(CLI) for f in [src, LIB, *hdrs]):
+        return CLI
+    cmd = ["g++", "-std=c++20", "-O2", f"-I{os.path.join(ROOT, 'include')}", f"-I{_json_include()}", src,
+           "-o", CLI, f"-L{OUT_DIR}", "-lkvp_b200", "-Wl,-rpath,$ORIGIN", "-pthread"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"CLI build failed:\n{r.stdout}\n{r.stderr}")
+    if verbose and r.stderr:
+        sys.stderr.write(r.stderr)
+    return CLI
+
+
 def up_to_date() -> bool:
     if not os.path.exists(LIB):
         return False
@@ -54,6 +81,7 @@ def up_to_date() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
+        build_cli(verbose)
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
@@ -63,6 +91,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    build_cli(verbose)
     return LIB
 
 

@@ -811,7 +811,7 @@ class PartitionLookupTable:
         import json
         try:
             with open(path, "w") as f:
-                json.dump(self.to_json(), f, indent=2)
+                json.dump(self.to_json(), f, indent=2, sort_keys=True)  # nlohmann::json key order
                 f.write("\n")
         except OSError as ex:
             raise IoError(f"cannot open table file for writing: {path}: {ex}")
