@@ -70,14 +70,20 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int STAGES = 4;
 constexpr int THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (2 per TMEM lane quarter)
 constexpr int EPI_WARPS = 8;
 
-template <int BN>
+// NCTA = 1: one CTA per 128 x BN tile.  NCTA = 2: a CTA pair (cluster of 2 on one TPC) per
+// 256 x BN tile -- each CTA loads its 128 A rows and HALF of the B columns, the leader issues
+// tcgen05.mma.cta_group::2 (M = 256) reading both CTAs' smem, each CTA's TMEM receives its own
+// 128 accumulator rows.  Per-SM smem traffic per FLOP drops by a third and the freed smem
+// buys 6 pipeline stages instead of 4.
+template <int BN, int NCTA>
 struct Cfg {
+    static constexpr int STAGES = NCTA == 2 ? 6 : 4;
+    static constexpr int B_ROWS = BN / NCTA;  // B rows this CTA loads per stage
     static constexpr uint32_t A_BYTES = BM * BK * 2;
-    static constexpr uint32_t B_BYTES = BN * BK * 2;
+    static constexpr uint32_t B_BYTES = B_ROWS * BK * 2;
     static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr uint32_t TMEM_COLS = 2 * BN;
     static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
@@ -271,12 +277,14 @@ __device__ __forceinline__ void resid_ssq_flush(const EpiArgs& ep, const ResidT&
     for (int i = 0; i < 8; ++i) ss[i] = 0.f;
 }
 
-template <int BN, int KIND>
+template <int BN, int KIND, int NCTA>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmBh, int M, int N, int K, int n_full, int group_m,
                    EpiArgs ep) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, NCTA>;
+    constexpr int STAGES = C::STAGES;
+    constexpr int TM = BM * NCTA;  // rows of one (pair) tile
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment by pointer arithmetic on the __shared__ array, so the compiler keeps
     // the shared state space (LDS/STS instead of generic loads/stores)
@@ -290,14 +298,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
+    const uint32_t rank = NCTA == 2 ? ptx::cluster_ctarank() : 0u;
+    const int unit = static_cast<int>(blockIdx.x) / NCTA, n_units = static_cast<int>(gridDim.x) / NCTA;
+    const int num_m = (M + TM - 1) / TM, num_n = (N + BN - 1) / BN;
     // Tiles [0, n_full) are BN wide; the remaining (last partial wave of) BN tiles run as two
     // BN/2-wide tiles each so the persistent grid's final round is evenly filled.  Only the
     // tile width changes, not the per-element K order: results are identical either way.
     const int num_tiles = n_full + 2 * (num_m * num_n - n_full);
     // Grouped rasterisation: tiles run in groups of `group_m` M-blocks, M-fastest inside a
     // group, so the CTAs in flight share a group_m x ~(148/group_m) block of the output: the
-    // group's A rows (group_m*BM*K*2 bytes, sized on the host to stay in L2) are read from
+    // group's A rows (group_m*TM*K*2 bytes, sized on the host to stay in L2) are read from
     // HBM once and each weight column block once per group.
     auto coords = [&](int big, int& m_blk, int& n_blk) {
         const int per_group = group_m * num_n;
@@ -331,13 +341,19 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(&tfull[b], 1);
-            ptx::mbar_init(&tempty[b], EPI_WARPS);
+            ptx::mbar_init(&tempty[b], EPI_WARPS * NCTA);  // both CTAs' epilogues free a buffer
         }
         ptx::fence_barrier_init();
     }
-    if (warp == 1) ptx::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+    if (warp == 1) {
+        if constexpr (NCTA == 2)
+            ptx::tmem_alloc_pair<C::TMEM_COLS>(tmem_slot);
+        else
+            ptx::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+    }
     ptx::tc_fence_before();
     __syncthreads();
+    if constexpr (NCTA == 2) ptx::cluster_sync();  // peer barriers initialised before any remote use
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -345,15 +361,26 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (int tile = unit; tile < num_tiles; tile += n_units) {
                 int m_blk, col_base, width;
                 decode(tile, m_blk, col_base, width);
                 const bool narrow = width != BN;
+                const uint32_t bytes = C::A_BYTES + (narrow ? C::B_BYTES / 2 : C::B_BYTES);
+                const int a_row = m_blk * TM + static_cast<int>(rank) * BM;
+                const int b_row = col_base + static_cast<int>(rank) * (width / NCTA);
                 for (int kb = 0; kb < num_kb; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    ptx::mbar_arrive_expect_tx(&full[stage], C::A_BYTES + (narrow ? C::B_BYTES / 2 : C::B_BYTES));
-                    ptx::tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
-                    ptx::tma_load_2d(sB + stage * C::B_BYTES, narrow ? &tmBh : &tmB, &full[stage], kb * BK, col_base);
+                    if constexpr (NCTA == 2) {
+                        // both CTAs' bytes land on the leader's stage barrier
+                        if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * bytes);
+                        const uint32_t bar = ptx::cluster_addr(&full[stage], 0);
+                        ptx::tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, bar, kb * BK, a_row);
+                        ptx::tma_load_2d_pair(sB + stage * C::B_BYTES, narrow ? &tmBh : &tmB, bar, kb * BK, b_row);
+                    } else {
+                        ptx::mbar_arrive_expect_tx(&full[stage], bytes);
+                        ptx::tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, a_row);
+                        ptx::tma_load_2d(sB + stage * C::B_BYTES, narrow ? &tmBh : &tmB, &full[stage], kb * BK, b_row);
+                    }
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -362,12 +389,12 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc_w = ptx::idesc_bf16(BM, BN), idesc_n = ptx::idesc_bf16(BM, BN / 2);
+        if (lane == 0 && rank == 0) {  // in a pair only the leader issues the MMAs
+            constexpr uint32_t idesc_w = ptx::idesc_bf16(TM, BN), idesc_n = ptx::idesc_bf16(TM, BN / 2);
             int stage = 0;
             uint32_t phase = 0;
             int t = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+            for (int tile = unit; tile < num_tiles; tile += n_units, ++t) {
                 int m_blk_u, col_base_u, width;
                 decode(tile, m_blk_u, col_base_u, width);
                 const uint32_t idesc = width == BN ? idesc_w : idesc_n;
@@ -384,15 +411,24 @@ __global__ void __launch_bounds__(THREADS, 1)
                     for (int k = 0; k < BK / 16; ++k) {
                         const uint64_t ad = ptx::smem_desc_sw128(a0 + k * 32, 16, 1024);
                         const uint64_t bd = ptx::smem_desc_sw128(b0 + k * 32, 16, 1024);
-                        ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                        if constexpr (NCTA == 2)
+                            ptx::mma_bf16_ss_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                        else
+                            ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
                     }
-                    ptx::mma_commit(&empty[stage]);
+                    if constexpr (NCTA == 2)
+                        ptx::mma_commit_pair(&empty[stage], 0x3);
+                    else
+                        ptx::mma_commit(&empty[stage]);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                ptx::mma_commit(&tfull[buf]);
+                if constexpr (NCTA == 2)
+                    ptx::mma_commit_pair(&tfull[buf], 0x3);
+                else
+                    ptx::mma_commit(&tfull[buf]);
             }
         }
     } else {
@@ -401,19 +437,21 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t quarter = warp & 3;
         const int half = (warp - 2) >> 2;
         constexpr int MY_MAX = BN / 64;  // 32-column chunks per warp group on a full-width tile
+        const uint32_t tempty_leader[2] = {NCTA == 2 ? ptx::cluster_addr(&tempty[0], 0) : 0u,
+                                           NCTA == 2 ? ptx::cluster_addr(&tempty[1], 0) : 0u};
         int t = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+        for (int tile = unit; tile < num_tiles; tile += n_units, ++t) {
             int m_blk, col_base, width;
             decode(tile, m_blk, col_base, width);
             const int MY = width / 64;
             const uint32_t buf = t & 1, aphase = (t >> 1) & 1;
-            const int64_t row = static_cast<int64_t>(m_blk) * BM + quarter * 32 + lane;
+            const int64_t row0 = static_cast<int64_t>(m_blk) * TM + rank * BM;  // this CTA's rows
+            const int64_t row = row0 + quarter * 32 + lane;
             const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + buf * BN;
-            float ssacc = 0.f;
             if constexpr (KIND == EPI_RESID) {
                 // The residual does not depend on the accumulator: fetch the first chunk of it
                 // while the tile's MMAs are still running, then one chunk ahead.
-                const ResidT rt{static_cast<int64_t>(m_blk) * BM + quarter * 32, lane >> 3, lane & 7};
+                const ResidT rt{row0 + quarter * 32, lane >> 3, lane & 7};
                 float* stg = reinterpret_cast<float*>(smem + STAGES * C::STAGE_BYTES + 256) + (warp - 2) * 1024;
                 float4 rv[8];
                 float ss[8];
@@ -460,61 +498,86 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tempty[buf]);
+            if (lane == 0) {
+                if constexpr (NCTA == 2)
+                    ptx::mbar_arrive_cluster(tempty_leader[buf]);
+                else
+                    ptx::mbar_arrive(&tempty[buf]);
+            }
         }
     }
     ptx::tc_fence_before();
     __syncthreads();
+    if constexpr (NCTA == 2) ptx::cluster_sync();  // the pair's TMEM and barriers outlive both CTAs' use
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+        if constexpr (NCTA == 2)
+            ptx::tmem_dealloc_pair<C::TMEM_COLS>(tmem_base);
+        else
+            ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
     }
 }
 
-template <int BN, int KIND>
+template <int BN, int KIND, int NCTA>
 void launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tbh, int M, int N, int K,
                const EpiArgs& ep, cudaStream_t s) {
-    auto kern = gemm_tc_kernel<BN, KIND>;
+    using Cf = Cfg<BN, NCTA>;
+    auto kern = gemm_tc_kernel<BN, KIND, NCTA>;
     static thread_local int configured_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
     if (configured_dev != dev) {  // attribute is per device; cheap to re-set
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::smem_for(KIND));
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::smem_for(KIND));
+        if (NCTA == 2) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
         configured_dev = dev;
     }
-    const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-    const int sms = num_sms();
-    const int grid = tiles < sms ? tiles : sms;
+    constexpr int TM = BM * NCTA;
+    const int tiles = ((M + TM - 1) / TM) * ((N + BN - 1) / BN);
+    const int units = num_sms() / NCTA;  // persistent: one CTA (pair) per SM (pair)
+    const int grid_units = tiles < units ? tiles : units;
     // split the last partial round into half-width tiles when they fit in one round
     static const bool split_tail = [] {
         const char* e = getenv("KVP_GEMM_TAIL");
         return !(e && e[0] == '0');
     }();
-    const int rem = tiles % grid;
-    const int n_full = (split_tail && BN == 256 && tiles > grid && rem > 0 && 2 * rem <= grid) ? tiles - rem : tiles;
+    const int rem = tiles % grid_units;
+    const int n_full =
+        (split_tail && BN == 256 && tiles > grid_units && rem > 0 && 2 * rem <= grid_units) ? tiles - rem : tiles;
     // M-blocks per raster group: keep the group's A rows within ~32 MB of L2
     static const int forced_group = [] {
         const char* e = getenv("KVP_GEMM_GROUP");
         return e ? atoi(e) : 0;
     }();
-    const int num_m = (M + BM - 1) / BM;
-    int group_m = forced_group > 0 ? forced_group : static_cast<int>((32ll << 20) / (static_cast<int64_t>(BM) * K * 2));
+    const int num_m = (M + TM - 1) / TM;
+    int group_m = forced_group > 0 ? forced_group : static_cast<int>((32ll << 20) / (static_cast<int64_t>(TM) * K * 2));
     group_m = group_m < 4 ? 4 : group_m;
     group_m = group_m > num_m ? num_m : group_m;
     note_launch();
-    kern<<<grid, THREADS, Cfg<BN>::smem_for(KIND), s>>>(ta, tb, tbh, M, N, K, n_full, group_m, ep);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid_units * NCTA));
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = Cf::smem_for(KIND);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = NCTA;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, ta, tb, tbh, M, N, K, n_full, group_m, ep);
 }
 
-template <int BN>
+template <int BN, int NCTA>
 void dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tbh, int M, int N, int K,
               const GemmEpilogue& g, cudaStream_t s) {
     EpiArgs ep{g.out0, g.ld0, g.n0, g.out1, g.ld1, g.n1, g.out2, g.ld2, g.outf, g.ldf, g.resid, g.ldr,
                g.outb, g.ldb, g.ssq_out, g.ssq_in, g.ssq_parts, g.norm_cols ? 1.0f / static_cast<float>(g.norm_cols) : 0.f};
     switch (g.kind) {
-        case EPI_QKV: launch_tc<BN, EPI_QKV>(ta, tb, tbh, M, N, K, ep, s); break;
-        case EPI_RESID: launch_tc<BN, EPI_RESID>(ta, tb, tbh, M, N, K, ep, s); break;
-        case EPI_RELU: launch_tc<BN, EPI_RELU>(ta, tb, tbh, M, N, K, ep, s); break;
-        default: launch_tc<BN, EPI_STORE>(ta, tb, tbh, M, N, K, ep, s); break;
+        case EPI_QKV: launch_tc<BN, EPI_QKV, NCTA>(ta, tb, tbh, M, N, K, ep, s); break;
+        case EPI_RESID: launch_tc<BN, EPI_RESID, NCTA>(ta, tb, tbh, M, N, K, ep, s); break;
+        case EPI_RELU: launch_tc<BN, EPI_RELU, NCTA>(ta, tb, tbh, M, N, K, ep, s); break;
+        default: launch_tc<BN, EPI_STORE, NCTA>(ta, tb, tbh, M, N, K, ep, s); break;
     }
 }
 
@@ -550,18 +613,27 @@ void gemm_bf16_tc(const bf16* A, int64_t M, int64_t K, const bf16* B, int64_t N,
         throw std::runtime_error("gemm_bf16_tc: K must be a multiple of 8 and operands 16-byte aligned");
     const int BN = gemm_bf16_tc_bn(M, N);
     const bool wide = BN == 256;
+    // CTA pairs for the wide tile whenever both CTAs of a pair get rows (KVP_GEMM_PAIR=0: off)
+    static const bool pair_ok = [] {
+        const char* e = getenv("KVP_GEMM_PAIR");
+        return !(e && e[0] == '0');
+    }();
+    const bool pair = wide && pair_ok && M > BM;
+    const uint32_t b_rows = static_cast<uint32_t>(BN / (pair ? 2 : 1));
     CUtensorMap ta, tb, tbh;
-    if (!make_tmap_bf16(&ta, A, K, M, K, BK, BM) || !make_tmap_bf16(&tb, B, K, N, K, BK, BN) ||
-        !make_tmap_bf16(&tbh, B, K, N, K, BK, BN / 2)) {
+    if (!make_tmap_bf16(&ta, A, K, M, K, BK, BM) || !make_tmap_bf16(&tb, B, K, N, K, BK, b_rows) ||
+        !make_tmap_bf16(&tbh, B, K, N, K, BK, b_rows / 2)) {
         char msg[160];
         snprintf(msg, sizeof msg, "cuTensorMapEncodeTiled failed (M=%lld N=%lld K=%lld)", (long long)M,
                  (long long)N, (long long)K);
         throw std::runtime_error(msg);
     }
-    if (wide)
-        dispatch<256>(ta, tb, tbh, (int)M, (int)N, (int)K, ep, s);
+    if (pair)
+        dispatch<256, 2>(ta, tb, tbh, (int)M, (int)N, (int)K, ep, s);
+    else if (wide)
+        dispatch<256, 1>(ta, tb, tbh, (int)M, (int)N, (int)K, ep, s);
     else
-        dispatch<128>(ta, tb, tbh, (int)M, (int)N, (int)K, ep, s);
+        dispatch<128, 1>(ta, tb, tbh, (int)M, (int)N, (int)K, ep, s);
 }
 
 }  // namespace kvp
