@@ -80,7 +80,7 @@ constexpr int EPI_WARPS = 8;
 // buys 6 pipeline stages instead of 4.
 template <int BN, int NCTA>
 struct Cfg {
-    static constexpr int STAGES = NCTA == 2 ? 6 : 4;
+    static constexpr int STAGES = NCTA == 2 ? (BN == 256 ? 6 : 8) : 4;
     static constexpr int B_ROWS = BN / NCTA;  // B rows this CTA loads per stage
     static constexpr uint32_t A_BYTES = BM * BK * 2;
     static constexpr uint32_t B_BYTES = B_ROWS * BK * 2;
@@ -437,8 +437,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t quarter = warp & 3;
         const int half = (warp - 2) >> 2;
         constexpr int MY_MAX = BN / 64;  // 32-column chunks per warp group on a full-width tile
-        const uint32_t tempty_leader[2] = {NCTA == 2 ? ptx::cluster_addr(&tempty[0], 0) : 0u,
-                                           NCTA == 2 ? ptx::cluster_addr(&tempty[1], 0) : 0u};
         int t = 0;
         for (int tile = unit; tile < num_tiles; tile += n_units, ++t) {
             int m_blk, col_base, width;
@@ -500,7 +498,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             __syncwarp();
             if (lane == 0) {
                 if constexpr (NCTA == 2)
-                    ptx::mbar_arrive_cluster(tempty_leader[buf]);
+                    ptx::mbar_arrive_cluster(ptx::cluster_addr(&tempty[buf], 0));
                 else
                     ptx::mbar_arrive(&tempty[buf]);
             }
@@ -583,23 +581,35 @@ void dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
 
 }  // namespace
 
+// CTA pairs whenever both CTAs of a pair get rows (KVP_GEMM_PAIR=0: single-CTA tiles only).
+static bool use_pair(int64_t M) {
+    static const bool pair_ok = [] {
+        const char* e = getenv("KVP_GEMM_PAIR");
+        return !(e && e[0] == '0');
+    }();
+    return pair_ok && M > BM;
+}
+
 int gemm_bf16_tc_bn(int64_t M, int64_t N) {
     // Tile width: BN=256 feeds the tensor core with the least smem traffic per FLOP; BN=128
-    // halves the tile so the persistent grid quantises better (e.g. 4096x4096 outputs are 512
-    // tiles = 3.46 waves of 148 SMs at BN=256 but 6.92 waves at BN=128).  Pick the width with
-    // the best (wave efficiency x per-tile efficiency); KVP_GEMM_BN=128|256 forces one.
+    // halves the tile so the persistent grid quantises better (e.g. 4096x4096 outputs are 256
+    // pair tiles = 3.46 waves of 74 SM pairs at BN=256 but 6.92 waves at BN=128).  Pick the
+    // width with the best (wave efficiency x per-tile efficiency); KVP_GEMM_BN=128|256 forces one.
     static const int forced = [] {
         const char* e = getenv("KVP_GEMM_BN");
         return e ? atoi(e) : 0;
     }();
-    const int sms = num_sms();
+    const bool pair = use_pair(M);
+    const int64_t tm = pair ? 2 * BM : BM;
+    const int units = num_sms() / (pair ? 2 : 1);
     auto score = [&](int64_t bn, double tile_eff) {
-        const int64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
-        const int64_t waves = (tiles + sms - 1) / sms;
-        const double useful = static_cast<double>(M) * N / (static_cast<double>(waves) * sms * BM * bn);
+        const int64_t tiles = ((M + tm - 1) / tm) * ((N + bn - 1) / bn);
+        const int64_t waves = (tiles + units - 1) / units;
+        const double useful = static_cast<double>(M) * N / (static_cast<double>(waves) * units * tm * bn);
         return useful * tile_eff;
     };
-    bool wide = score(256, 1.0) >= score(128, 0.72);  // BN=128 tiles measured ~25% slower per FLOP
+    // per-FLOP efficiency of the narrow tile relative to BN=256 (measured)
+    bool wide = score(256, 1.0) >= score(128, pair ? 0.65 : 0.72);
     if (N < 256) wide = false;
     if (forced == 128) wide = false;
     if (forced == 256 && N >= 256) wide = true;
@@ -613,12 +623,7 @@ void gemm_bf16_tc(const bf16* A, int64_t M, int64_t K, const bf16* B, int64_t N,
         throw std::runtime_error("gemm_bf16_tc: K must be a multiple of 8 and operands 16-byte aligned");
     const int BN = gemm_bf16_tc_bn(M, N);
     const bool wide = BN == 256;
-    // CTA pairs for the wide tile whenever both CTAs of a pair get rows (KVP_GEMM_PAIR=0: off)
-    static const bool pair_ok = [] {
-        const char* e = getenv("KVP_GEMM_PAIR");
-        return !(e && e[0] == '0');
-    }();
-    const bool pair = wide && pair_ok && M > BM;
+    const bool pair = use_pair(M);
     const uint32_t b_rows = static_cast<uint32_t>(BN / (pair ? 2 : 1));
     CUtensorMap ta, tb, tbh;
     if (!make_tmap_bf16(&ta, A, K, M, K, BK, BM) || !make_tmap_bf16(&tb, B, K, N, K, BK, b_rows) ||
@@ -629,11 +634,11 @@ void gemm_bf16_tc(const bf16* A, int64_t M, int64_t K, const bf16* B, int64_t N,
         throw std::runtime_error(msg);
     }
     if (pair)
-        dispatch<256, 2>(ta, tb, tbh, (int)M, (int)N, (int)K, ep, s);
-    else if (wide)
-        dispatch<256, 1>(ta, tb, tbh, (int)M, (int)N, (int)K, ep, s);
+        wide ? dispatch<256, 2>(ta, tb, tbh, (int)M, (int)N, (int)K, ep, s)
+             : dispatch<128, 2>(ta, tb, tbh, (int)M, (int)N, (int)K, ep, s);
     else
-        dispatch<128, 1>(ta, tb, tbh, (int)M, (int)N, (int)K, ep, s);
+        wide ? dispatch<256, 1>(ta, tb, tbh, (int)M, (int)N, (int)K, ep, s)
+             : dispatch<128, 1>(ta, tb, tbh, (int)M, (int)N, (int)K, ep, s);
 }
 
 }  // namespace kvp
