@@ -161,6 +161,12 @@ kvp_status kvp_engine_profile_layer(kvp_engine* e, int64_t rows, int64_t offset,
 kvp_status kvp_bench_gemm(kvp_engine* e, int64_t M, int64_t N, int64_t K, int32_t epi, int32_t reps, float* ms,
                           int32_t* bn_out);
 
+/* Kernel microbenchmark: the bf16 prefix-causal attention of q_rows queries at absolute
+ * positions [offset, offset + q_rows) over offset + q_rows keys (random bf16 Q/K/V, head_dim
+ * 64 or 128) on devices[0]; median device ms over reps (CUDA events). */
+kvp_status kvp_bench_attn(kvp_engine* e, int64_t q_rows, int64_t offset, int32_t n_heads, int32_t n_kv_heads,
+                          int32_t head_dim, int32_t reps, float* ms);
+
 /* ------------------------------------------- one rank of a multi-process run */
 /* One process per GPU: the caller owns the transport (e.g. NCCL p2p via torch.distributed)
  * and drives one rank's per-layer schedule -- the worker loop of run<T>

@@ -3,7 +3,8 @@
 // Reference: causal_attention (model.hpp:112-158).  One CTA owns TWO 128-query tiles (a, b)
 // of one head -- absolute positions offset + q0 ... offset + q0 + 255 -- and walks the
 // 128-key tiles [0, offset + last query]; each K/V tile is loaded once for both query tiles.
-//   warp 0      TMA producer: Q_a, Q_b once, then K/V tiles through a 2-stage smem ring;
+//   warp 0      TMA producer: Q_a, Q_b once, then K and V tiles through separate smem rings
+//               (K runs a stage ahead: it is released as soon as both S MMAs have read it);
 //   warp 1      MMA issuer (one lane) + TMEM owner, ping-pong between the tiles:
 //                 S_x = Q_x K_j^T  (SS: A=Q smem, B=K smem, both K-major SW128) -> TMEM S_x
 //                 O_x += P_x V_j   (TS: A=P_x in TMEM, packed bf16 over S_x; B=V smem MN-major)
@@ -17,6 +18,7 @@
 // Key tiles are aligned to absolute key 0, fully masked tiles are skipped per query tile and
 // rows are independent, so results are bitwise independent of how the context is split over
 // ranks (Serial == TSP == KVR).
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <stdexcept>
@@ -33,16 +35,26 @@ namespace {
 
 constexpr int BQ = 128;   // queries per tile (two tiles per CTA)
 constexpr int BKV = 128;  // keys per tile
-constexpr int THREADS = 576;  // warp 0 TMA, warp 1 MMA, warps 2..17 softmax (8 per query tile)
+constexpr int THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 softmax
 constexpr uint32_t TMEM_COLS = 512;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units: p <= 2^8 between rescales
+constexpr int DEFAULT_POLY_128 = 0;        // exp2 column pairs (of 16) on the FMA pipe
+constexpr int DEFAULT_POLY_64 = 0;
 
+// K and V tiles have separate smem rings: K(j) is released as soon as both S MMAs of key
+// tile j are done, so K(j+1..) streams in while the softmax of tile j runs.
 template <int HD>
 struct ACfg {
     static constexpr int HALVES = HD / 64;  // 64-wide (128 B) TMA boxes
     static constexpr uint32_t Q_BYTES = BQ * HD * 2;
     static constexpr uint32_t KV_BYTES = BKV * HD * 2;
-    static constexpr uint32_t SMEM = 2 * Q_BYTES + 4 * KV_BYTES + 1024 + 256 + 6144;  // + row-max/sum exchange
+    static constexpr int KST = HD == 64 ? 4 : 3;  // K stages
+    static constexpr int VST = HD == 64 ? 3 : 2;  // V stages
+    static constexpr uint32_t XCH = 0;
+    static constexpr uint32_t NEED = 2 * Q_BYTES + (KST + VST) * KV_BYTES + 256 + XCH;
+    // + up to 1 KB of slack for aligning the dynamic smem base to 1024 B (the SW128 atoms)
+    static constexpr uint32_t SMEM = NEED + 1024 <= 232448 ? NEED + 1024 : 232448;
+    static_assert(NEED + 512 <= 232448, "attention smem over the 227 KB opt-in limit");
 };
 
 // ---- packed f32x2 arithmetic (sm_100: FFMA2 / FADD2) and exp2 on two pipes ----
@@ -95,30 +107,44 @@ struct AttnArgs {
     int n_heads, group;
     int64_t ldo;
     bf16* O;
-    float sl2;  // softmax scale * log2(e)
+    float sl2;     // softmax scale * log2(e)
+    int mma_wait;  // 1: the MMA issuer waits for PV(j) before S(j+1) reuses its TMEM columns
+    uint32_t* trace;  // tuning only (KVP_ATTN_TRACE): SM clock of pipeline events of one CTA
+    int trace_blk;
 };
 
-template <int HD, int POLY_FROM>
+// trace[ev * 512 + j] = clock() of event ev for key tile j, CTA (blockIdx.y * gridDim.x + blockIdx.x) == trace_blk
+#define ATTN_TRACE(ev, j)                                                                              \
+    do {                                                                                               \
+        if (a.trace && static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x) == a.trace_blk && (j) < 512) \
+            a.trace[(ev) * 512 + (j)] = static_cast<uint32_t>(clock());                                \
+    } while (0)
+
+template <int HD, int NPOLY>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
     using C = ACfg<HD>;
+    constexpr int KST = C::KST, VST = C::VST;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment by pointer arithmetic on the __shared__ array, so the compiler keeps
     // the shared state space (LDS/STS instead of generic loads/stores)
-    uint8_t* smem = smem_raw + ((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u);
+    const uint32_t pad = (1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u;
+    if (pad + C::NEED > C::SMEM) __trap();  // dynamic smem base too far from 1 KB alignment
+    uint8_t* smem = smem_raw + pad;
     uint8_t* sQ = smem;                  // [2] query tiles
-    uint8_t* sK = sQ + 2 * C::Q_BYTES;   // [2] stages
-    uint8_t* sV = sK + 2 * C::KV_BYTES;  // [2] stages
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sV + 2 * C::KV_BYTES);
+    uint8_t* sK = sQ + 2 * C::Q_BYTES;     // [KST] stages
+    uint8_t* sV = sK + KST * C::KV_BYTES;  // [VST] stages
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sV + VST * C::KV_BYTES);
     uint64_t* q_full = bar;
-    uint64_t* k_full = bar + 1;    // [2] stages
-    uint64_t* v_full = bar + 3;    // [2] stages
-    uint64_t* kv_empty = bar + 5;  // [2] stages
-    uint64_t* s_full = bar + 7;    // [2] query tiles
-    uint64_t* p_full = bar + 9;    // [2] query tiles
-    uint64_t* o_done = bar + 11;   // [2] query tiles
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
+    uint64_t* k_full = bar + 1;              // [KST]
+    uint64_t* k_empty = k_full + KST;        // [KST]
+    uint64_t* v_full = k_empty + KST;        // [VST]
+    uint64_t* v_empty = v_full + VST;        // [VST]
+    uint64_t* s_full = v_empty + VST;        // [2] query tiles
+    uint64_t* p_full = s_full + 2;           // [2] query tiles
+    uint64_t* o_done = p_full + 2;           // [2] query tiles
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int num_pairs = static_cast<int>((a.q_rows + 2 * BQ - 1) / (2 * BQ));
@@ -140,12 +166,17 @@ __global__ void __launch_bounds__(THREADS, 1)
         ptx::tma_prefetch_desc(&tmK);
         ptx::tma_prefetch_desc(&tmV);
         ptx::mbar_init(q_full, 1);
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < KST; ++s) {
             ptx::mbar_init(&k_full[s], 1);
+            ptx::mbar_init(&k_empty[s], 1);
+        }
+        for (int s = 0; s < VST; ++s) {
             ptx::mbar_init(&v_full[s], 1);
-            ptx::mbar_init(&kv_empty[s], 1);
+            ptx::mbar_init(&v_empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(&s_full[s], 1);
-            ptx::mbar_init(&p_full[s], 8);
+            ptx::mbar_init(&p_full[s], 4);  // the 4 softmax warps of the tile
             ptx::mbar_init(&o_done[s], 1);
         }
         ptx::fence_barrier_init();
@@ -163,15 +194,23 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (int hv = 0; hv < C::HALVES; ++hv)
                     ptx::tma_load_2d(sQ + x * C::Q_BYTES + hv * BQ * 128, &tmQ, q_full, h * HD + hv * 64,
                                      static_cast<int32_t>(q0 + x * BQ));
+            // K(t), V(t) in need order; K(t) waits for both S MMAs of tile t - KST, V(t) for both
+            // PV MMAs of tile t - VST, so K runs a stage further ahead (blocking waits: the
+            // producer lane never spins on the issue slots of the softmax warps of its SMSP)
             for (int t = 0; t < n_kt[1]; ++t) {
-                const int s = t & 1;
-                ptx::mbar_wait(&kv_empty[s], ((t >> 1) & 1) ^ 1);
-                ptx::mbar_arrive_expect_tx(&k_full[s], C::KV_BYTES);
+                const int sk = t % KST, sv = t % VST;
+                ptx::mbar_wait(&k_empty[sk], ((t / KST) & 1) ^ 1);
+                ATTN_TRACE(12, t);
+                ptx::mbar_arrive_expect_tx(&k_full[sk], C::KV_BYTES);
                 for (int hv = 0; hv < C::HALVES; ++hv)
-                    ptx::tma_load_2d(sK + s * C::KV_BYTES + hv * BKV * 128, &tmK, &k_full[s], g * HD + hv * 64, t * BKV);
-                ptx::mbar_arrive_expect_tx(&v_full[s], C::KV_BYTES);
+                    ptx::tma_load_2d(sK + sk * C::KV_BYTES + hv * BKV * 128, &tmK, &k_full[sk], g * HD + hv * 64,
+                                     t * BKV);
+                ptx::mbar_wait(&v_empty[sv], ((t / VST) & 1) ^ 1);
+                ATTN_TRACE(13, t);
+                ptx::mbar_arrive_expect_tx(&v_full[sv], C::KV_BYTES);
                 for (int hv = 0; hv < C::HALVES; ++hv)
-                    ptx::tma_load_2d(sV + s * C::KV_BYTES + hv * BKV * 128, &tmV, &v_full[s], g * HD + hv * 64, t * BKV);
+                    ptx::tma_load_2d(sV + sv * C::KV_BYTES + hv * BKV * 128, &tmV, &v_full[sv], g * HD + hv * 64,
+                                     t * BKV);
             }
         }
     } else if (warp == 1) {
@@ -179,9 +218,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             constexpr uint32_t idesc_s = ptx::idesc_bf16(BQ, BKV, 0);
             constexpr uint32_t idesc_o = ptx::idesc_bf16(BQ, HD, 1);  // B = V is MN-major
             auto issue_s = [&](int x, int t) {
-                const int s = t & 1;
-                ptx::mbar_wait(&k_full[s], (t >> 1) & 1);
+                const int s = t % KST;
+                ptx::mbar_wait(&k_full[s], (t / KST) & 1);
                 ptx::tc_fence_after();
+                ATTN_TRACE(0 + x, t);
                 const uint32_t q_addr = ptx::smem_u32(sQ + x * C::Q_BYTES);
                 const uint32_t k_addr = ptx::smem_u32(sK + s * C::KV_BYTES);
 #pragma unroll
@@ -192,12 +232,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                     ptx::mma_bf16_ss(tmem + x * 128, ad, bd, idesc_s, k != 0);
                 }
                 ptx::mma_commit(&s_full[x]);
+                if (x == 1) ptx::mma_commit(&k_empty[s]);  // tile b is the last reader of K(t)
             };
             auto issue_pv = [&](int x, int t) {
-                const int s = t & 1;
+                const int s = t % VST;
                 ptx::mbar_wait(&p_full[x], t & 1);
-                ptx::mbar_wait(&v_full[s], (t >> 1) & 1);
+                ptx::mbar_wait(&v_full[s], (t / VST) & 1);
                 ptx::tc_fence_after();
+                ATTN_TRACE(2 + x, t);
                 const uint32_t v_addr = ptx::smem_u32(sV + s * C::KV_BYTES);
 #pragma unroll
                 for (int k = 0; k < BKV / 16; ++k) {
@@ -207,6 +249,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     ptx::mma_bf16_ts(tmem + 256 + x * 128, tmem + x * 128 + k * 8, bd, idesc_o, (t | k) != 0);
                 }
                 ptx::mma_commit(&o_done[x]);
+                if (x == 1) ptx::mma_commit(&v_empty[s]);  // tile b is the last reader of V(t)
             };
             ptx::mbar_wait(q_full, 0);
             issue_s(0, 0);
@@ -215,102 +258,48 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (j < n_kt[0]) {
                     issue_pv(0, j);
                     if (j + 1 < n_kt[0]) {
-                        ptx::mbar_wait(&o_done[0], j & 1);  // S_a held P_a(j)
+                        // S_a(j+1) overwrites the TMEM columns P_a(j) is read from: tcgen05.mma
+                        // ops of one thread execute in issue order, so waiting for PV_a(j) is
+                        // only needed when the pipeline is not trusted (a.mma_wait)
+                        if (a.mma_wait) ptx::mbar_wait(&o_done[0], j & 1);
                         issue_s(0, j + 1);
                     }
                 }
                 issue_pv(1, j);
-                ptx::mma_commit(&kv_empty[j & 1]);  // tile b is the last reader of stage j%2
                 if (j + 1 < n_kt[1]) {
-                    ptx::mbar_wait(&o_done[1], j & 1);
+                    if (a.mma_wait) ptx::mbar_wait(&o_done[1], j & 1);
                     issue_s(1, j + 1);
                 }
             }
         }
     } else {
-        // 16 softmax warps: 8 per query tile; the two warps of a TMEM lane quarter split the
-        // tile's 128 key columns (and the O columns) and exchange row max / row sum through smem.
-        const int sw = warp - 2;
-        const int x = sw >> 3;                // query tile
-        const int sub = (sw >> 2) & 1;        // key half (and O half) of this warp
-        const uint32_t quarter = warp & 3;    // TMEM lane quarter this warp may access
-        constexpr int KC = BKV / 2, OC = HD / 2;
+        // 8 softmax warps: warps 2..5 own tile a, warps 6..9 tile b; warp w reads TMEM lane
+        // quarter w % 4, one thread per query row (all 128 keys of the tile, no exchange).
+        const int x = (warp - 2) >> 2;                         // query tile
+        const uint32_t quarter = warp & 3;                     // TMEM lane quarter this warp may access
         const int xrow = static_cast<int>(quarter) * 32 + lane;
         const int64_t row = q0 + x * BQ + xrow;
-        const int64_t abs_row = a.offset + row;
+        const int abs_row = static_cast<int>(a.offset + row);  // positions < 2^31 (host-checked)
+        const int tile_first_abs = abs_row - xrow;
         const uint32_t lane_base = tmem + ((quarter * 32u) << 16);
-        const uint32_t s_col = x * 128 + sub * KC;        // fp32 S columns of my key half
-        const uint32_t p_col = x * 128 + sub * (KC / 2);  // packed bf16 P columns of my key half
-        const uint32_t o_col = 256 + x * 128 + sub * OC;
-        float* xch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bar) + 256);  // [2 par][2 x][2 sub][128]
-        const uint32_t bar_id = 1 + x * 4 + quarter;      // named barrier of the two partner warps
         const int nt = n_kt[x];
-        const int64_t tile_first_abs = a.offset + q0 + x * BQ;
+        const float2 sl2v = make_float2(a.sl2, a.sl2);
         float m_run = -INFINITY, l = 0.f;
-        for (int j = 0; j < nt; ++j) {
-            ptx::mbar_wait(&s_full[x], j & 1);
-            ptx::tc_fence_after();
-            float sv[KC];
-#pragma unroll
-            for (int c = 0; c < KC / 32; ++c) {
-                uint32_t r[32];
-                ptx::tmem_ld32(lane_base + s_col + c * 32, r);
-                ptx::tmem_ld_wait();
-#pragma unroll
-                for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(r[i]);
-            }
-            const int64_t key0 = static_cast<int64_t>(j) * BKV + sub * KC;  // first key of my half
-            const bool diag = static_cast<int64_t>(j) * BKV + BKV - 1 > tile_first_abs;
-            if (diag) {
-                // keys [key0, key0 + nvis) are visible to this row; 32-bit compares against
-                // compile-time column indices, applied only on the diagonal tile
-                const int64_t v = abs_row - key0 + 1;
-                const int nvis = v < 0 ? 0 : (v > KC ? KC : static_cast<int>(v));
-#pragma unroll
-                for (int i = 0; i < KC; ++i) sv[i] = i < nvis ? sv[i] : -INFINITY;
-            }
-            float mx = -INFINITY;
-#pragma unroll
-            for (int i = 0; i < KC; ++i) mx = fmaxf(mx, sv[i]);
-            float* xb = xch + (j & 1) * 512 + x * 256;
-            xb[sub * 128 + xrow] = mx;
-            asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-            mx = fmaxf(mx, xb[(sub ^ 1) * 128 + xrow]);  // row max over all 128 keys
-            mx *= a.sl2;                                   // scale > 0: max commutes with it
-            const bool need = mx > m_run + RESCALE_THRESHOLD;
-            if (__any_sync(0xffffffffu, need)) {
-                const float m_new = need ? mx : m_run;
-                const float alpha = need ? exp2f(m_run - m_new) : 1.0f;
-                if (j > 0) {
-                    ptx::mbar_wait(&o_done[x], (j - 1) & 1);
-                    ptx::tc_fence_after();
-#pragma unroll
-                    for (int c = 0; c < OC / 16; ++c) {
-                        uint32_t r[16];
-                        ptx::tmem_ld16(lane_base + o_col + c * 16, r);
-                        ptx::tmem_ld_wait();
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-                        ptx::tmem_st16(lane_base + o_col + c * 16, r);
-                    }
-                    ptx::tmem_st_wait();
-                }
-                l *= alpha;
-                m_run = m_new;
-            }
-            const float nbv = (m_run == -INFINITY) ? 0.f : -m_run;
-            const float2 sl2v = make_float2(a.sl2, a.sl2), nb2 = make_float2(nbv, nbv);
+        // exp2 of the row's 128 scores against base m (log2 units), P -> TMEM as packed bf16
+        // over the first 64 S columns; returns the row sum of P
+        auto exp_store = [&](const float (&sv)[BKV], float m, bool diag) -> float {
+            const float2 nb2 = make_float2(-m, -m);
             float2 lacc = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int c = 0; c < KC / 32; ++c) {
+            for (int c = 0; c < BKV / 32; ++c) {
                 uint32_t pk[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const int col = c * 32 + 2 * i;
-                    const int gcol = sub * KC + col;  // the exp2 unit depends on the key column only
                     const float2 xv = ffma2(make_float2(sv[col], sv[col + 1]), sl2v, nb2);
                     float2 pv;
-                    if (gcol >= POLY_FROM) {
+                    // NPOLY of every 16 column pairs take exp2 on the FMA pipe, the rest on MUFU
+                    if (i >= 16 - NPOLY) {
                         pv = ex2_poly2(xv);
                         if (diag) {  // the FMA-pipe exp2 clamps -inf: zero masked keys
                             pv.x = sv[col] == -INFINITY ? 0.f : pv.x;
@@ -323,27 +312,84 @@ __global__ void __launch_bounds__(THREADS, 1)
                     lacc = fadd2(lacc, pv);
                     pk[i] = ptx::pack_bf16(pv.x, pv.y);
                 }
-                ptx::tmem_st16(lane_base + p_col + c * 16, pk);  // P over S, packed bf16
+                ptx::tmem_st16(lane_base + x * 128 + c * 16, pk);
             }
-            l += lacc.x + lacc.y;
+            return lacc.x + lacc.y;
+        };
+        for (int j = 0; j < nt; ++j) {
+            ptx::mbar_wait(&s_full[x], j & 1);
+            ptx::tc_fence_after();
+            const bool tr = quarter == 0 && lane == 0;
+            if (tr) ATTN_TRACE(4 + x, j);
+            float sv[BKV];
+            {
+                uint32_t r[BKV / 32][32];
+#pragma unroll
+                for (int c = 0; c < BKV / 32; ++c) ptx::tmem_ld32(lane_base + x * 128 + c * 32, r[c]);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int c = 0; c < BKV / 32; ++c)
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(r[c][i]);
+            }
+            if (tr) ATTN_TRACE(6 + x, j);
+            const bool diag = j * BKV + BKV - 1 > tile_first_abs;
+            if (diag) {
+                // keys [j*BKV, j*BKV + nvis) are visible to this row; 32-bit compares against
+                // compile-time column indices, applied only on the diagonal tile
+                const int v = abs_row - j * BKV + 1;
+                const int nvis = v < 0 ? 0 : (v > BKV ? BKV : v);
+#pragma unroll
+                for (int i = 0; i < BKV; ++i) sv[i] = i < nvis ? sv[i] : -INFINITY;
+            }
+            float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+            for (int i = 0; i < BKV; i += 8) {
+                m4[0] = fmaxf(m4[0], fmaxf(sv[i + 0], sv[i + 4]));
+                m4[1] = fmaxf(m4[1], fmaxf(sv[i + 1], sv[i + 5]));
+                m4[2] = fmaxf(m4[2], fmaxf(sv[i + 2], sv[i + 6]));
+                m4[3] = fmaxf(m4[3], fmaxf(sv[i + 3], sv[i + 7]));
+            }
+            const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * a.sl2;  // scale > 0
+            if (tr) ATTN_TRACE(8 + x, j);
+            const bool need = mx > m_run + RESCALE_THRESHOLD;
+            if (__any_sync(0xffffffffu, need)) {
+                const float m_new = need ? mx : m_run;
+                const float alpha = need ? exp2f(m_run - m_new) : 1.0f;
+                if (j > 0) {
+                    ptx::mbar_wait(&o_done[x], (j - 1) & 1);
+                    ptx::tc_fence_after();
+#pragma unroll
+                    for (int c = 0; c < HD / 16; ++c) {
+                        uint32_t r[16];
+                        ptx::tmem_ld16(lane_base + 256 + x * 128 + c * 16, r);
+                        ptx::tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+                        ptx::tmem_st16(lane_base + 256 + x * 128 + c * 16, r);
+                    }
+                    ptx::tmem_st_wait();
+                }
+                l *= alpha;
+                m_run = m_new;
+            }
+            const float lsum = exp_store(sv, m_run, diag);
+            l += lsum;
             ptx::tmem_st_wait();
             ptx::tc_fence_before();
             __syncwarp();
+            if (tr) ATTN_TRACE(10 + x, j);
             if (lane == 0) ptx::mbar_arrive(&p_full[x]);
         }
-        // epilogue: O / (l_0 + l_1) -> bf16, each warp its O half
-        float* lb = xch + 1024 + x * 256;
-        lb[sub * 128 + xrow] = l;
-        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-        const float lo = lb[xrow], hi = lb[128 + xrow];
-        const float inv = 1.0f / (lo + hi);  // same order on both partners
+        // epilogue: O / l -> bf16
+        const float inv = 1.0f / l;
         ptx::mbar_wait(&o_done[x], (nt - 1) & 1);
         ptx::tc_fence_after();
-        bf16* orow = a.O + row * a.ldo + static_cast<int64_t>(h) * HD + sub * OC;
+        bf16* orow = a.O + row * a.ldo + static_cast<int64_t>(h) * HD;
 #pragma unroll
-        for (int c = 0; c < OC / 32; ++c) {
+        for (int c = 0; c < HD / 32; ++c) {
             uint32_t r[32];
-            ptx::tmem_ld32(lane_base + o_col + c * 32, r);
+            ptx::tmem_ld32(lane_base + 256 + x * 128 + c * 32, r);
             ptx::tmem_ld_wait();
             if (row < a.q_rows) {
 #pragma unroll
@@ -366,7 +412,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 }
 
-template <int HD, int POLY_FROM>
+int mma_wait_flag() {
+    static const int w = [] {
+        const char* e = getenv("KVP_ATTN_MMA_WAIT");
+        return e ? atoi(e) : 0;
+    }();
+    return w;
+}
+
+template <int HD, int NPOLY>
 void launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShape& sh, cudaStream_t s) {
     CUtensorMap tq, tk, tv;
     if (!make_tmap_bf16(&tq, Q, static_cast<uint64_t>(sh.n_heads) * HD, sh.q_rows, sh.ldq, 64, BQ) ||
@@ -377,15 +431,44 @@ void launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShap
     int dev = 0;
     cudaGetDevice(&dev);
     if (configured != dev) {
-        cudaFuncSetAttribute(attn_tc_kernel<HD, POLY_FROM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(attn_tc_kernel<HD, NPOLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              ACfg<HD>::SMEM);
         configured = dev;
     }
     AttnArgs a{sh.q_rows, sh.k_rows, sh.offset, sh.n_heads, sh.n_heads / sh.n_kv_heads, sh.ldo, O,
-               (1.0f / sqrtf(static_cast<float>(HD))) * 1.4426950408889634f};
+               (1.0f / sqrtf(static_cast<float>(HD))) * 1.4426950408889634f, mma_wait_flag(), nullptr, -1};
+    // tuning only: KVP_ATTN_TRACE=<cta> records one CTA's pipeline events into KVP_ATTN_TRACE_OUT
+    static const char* trace_env = getenv("KVP_ATTN_TRACE");
+    if (trace_env) {
+        static uint32_t* buf = nullptr;
+        if (!buf) cudaMalloc(&buf, 16 * 512 * sizeof(uint32_t));
+        cudaMemsetAsync(buf, 0, 16 * 512 * sizeof(uint32_t), s);
+        a.trace = buf;
+        a.trace_blk = atoi(trace_env);
+    }
     dim3 grid(static_cast<unsigned>(sh.n_heads), static_cast<unsigned>((sh.q_rows + 2 * BQ - 1) / (2 * BQ)));
     note_launch();
-    attn_tc_kernel<HD, POLY_FROM><<<grid, THREADS, ACfg<HD>::SMEM, s>>>(tq, tk, tv, a);
+    attn_tc_kernel<HD, NPOLY><<<grid, THREADS, ACfg<HD>::SMEM, s>>>(tq, tk, tv, a);
+    if (a.trace) {
+        uint32_t host[16 * 512];
+        cudaMemcpyAsync(host, a.trace, sizeof(host), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        const char* out = getenv("KVP_ATTN_TRACE_OUT");
+        if (FILE* f = fopen(out ? out : "attn_trace.bin", "wb")) {
+            fwrite(host, sizeof(host), 1, f);
+            fclose(f);
+        }
+    }
+}
+
+template <int HD>
+void launch_poly(int np, const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShape& sh, cudaStream_t s) {
+    switch (np) {
+        case 0: launch<HD, 0>(Q, K, V, O, sh, s); break;
+        case 2: launch<HD, 2>(Q, K, V, O, sh, s); break;
+        case 4: launch<HD, 4>(Q, K, V, O, sh, s); break;
+        default: throw std::runtime_error("attn_tc: KVP_ATTN_POLY must be 0, 2 or 4");
+    }
 }
 
 }  // namespace
@@ -394,19 +477,16 @@ bool attn_tc_supported(int head_dim) { return head_dim == 64 || head_dim == 128;
 
 void attn_bf16_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShape& sh, cudaStream_t s) {
     if (sh.q_rows <= 0) return;
-    // KVP_ATTN_POLY = number of key columns (of 128) whose exp2 runs on the FMA pipe
+    // KVP_ATTN_POLY = column pairs (of every 16) whose exp2 runs on the FMA pipe
     static const int poly = [] {
         const char* e = getenv("KVP_ATTN_POLY");
-        return e ? atoi(e) : 0;
+        return e ? atoi(e) : -1;
     }();
     if (sh.head_dim != 128 && sh.head_dim != 64) throw std::runtime_error("attn_tc: head_dim must be 64 or 128");
+    if (sh.offset + sh.q_rows + BKV >= (int64_t(1) << 31)) throw std::runtime_error("attn_tc: positions must be < 2^31");
     const bool h128 = sh.head_dim == 128;
-    switch (poly) {
-        case 48: h128 ? launch<128, 80>(Q, K, V, O, sh, s) : launch<64, 80>(Q, K, V, O, sh, s); break;
-        case 64: h128 ? launch<128, 64>(Q, K, V, O, sh, s) : launch<64, 64>(Q, K, V, O, sh, s); break;
-        case 32: h128 ? launch<128, 96>(Q, K, V, O, sh, s) : launch<64, 96>(Q, K, V, O, sh, s); break;
-        default: h128 ? launch<128, 128>(Q, K, V, O, sh, s) : launch<64, 128>(Q, K, V, O, sh, s); break;
-    }
+    const int np = poly >= 0 ? poly : (h128 ? DEFAULT_POLY_128 : DEFAULT_POLY_64);
+    h128 ? launch_poly<128>(np, Q, K, V, O, sh, s) : launch_poly<64>(np, Q, K, V, O, sh, s);
 }
 
 }  // namespace kvp

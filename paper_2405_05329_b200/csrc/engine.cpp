@@ -1167,6 +1167,59 @@ kvp_status kvp_bench_gemm(kvp_engine* e, int64_t M, int64_t N, int64_t K, int32_
     });
 }
 
+kvp_status kvp_bench_attn(kvp_engine* e, int64_t q_rows, int64_t offset, int32_t n_heads, int32_t n_kv_heads,
+                          int32_t head_dim, int32_t reps, float* ms) {
+    return guard([&] {
+        if (!e || !ms) throw Error(KVP_ERR_INPUT, "null argument");
+        if (q_rows < 1 || offset < 0 || reps < 1 || n_heads < 1 || n_kv_heads < 1 || n_heads % n_kv_heads)
+            throw Error(KVP_ERR_INPUT, "bad attention shape");
+        if (!attn_tc_supported(head_dim)) throw Error(KVP_ERR_INPUT, "head_dim must be 64 or 128");
+        std::lock_guard<std::mutex> g(e->mu);
+        KVP_CUDA(cudaSetDevice(e->devices[0]));
+        const int64_t k_rows = offset + q_rows, qd = int64_t(n_heads) * head_dim, kvd = int64_t(n_kv_heads) * head_dim;
+        DevBuf q, k, v, o, tmp;
+        q.ensure(q_rows * qd * 2, e->devices[0]);
+        k.ensure(k_rows * kvd * 2, e->devices[0]);
+        v.ensure(k_rows * kvd * 2, e->devices[0]);
+        o.ensure(q_rows * qd * 2, e->devices[0]);
+        tmp.ensure(std::max(q_rows * qd, k_rows * kvd) * 4, e->devices[0]);
+        cudaStream_t st = nullptr;
+        launch_seeded_f32(tmp.as<float>(), q_rows, qd, 2.0, 21, st);
+        launch_cast_bf16(tmp.as<float>(), q.as<bf16>(), q_rows * qd, st);
+        launch_seeded_f32(tmp.as<float>(), k_rows, kvd, 2.0, 22, st);
+        launch_cast_bf16(tmp.as<float>(), k.as<bf16>(), k_rows * kvd, st);
+        launch_seeded_f32(tmp.as<float>(), k_rows, kvd, 1.0, 23, st);
+        launch_cast_bf16(tmp.as<float>(), v.as<bf16>(), k_rows * kvd, st);
+        AttnShape sh;
+        sh.q_rows = q_rows;
+        sh.k_rows = k_rows;
+        sh.offset = offset;
+        sh.n_heads = n_heads;
+        sh.n_kv_heads = n_kv_heads;
+        sh.head_dim = head_dim;
+        sh.ldq = qd;
+        sh.ldkv = kvd;
+        sh.ldo = qd;
+        cudaEvent_t e0, e1;
+        KVP_CUDA(cudaEventCreate(&e0));
+        KVP_CUDA(cudaEventCreate(&e1));
+        std::vector<float> t;
+        for (int i = 0; i < reps + 1; ++i) {
+            KVP_CUDA(cudaEventRecord(e0, st));
+            attn_bf16(q.as<bf16>(), k.as<bf16>(), v.as<bf16>(), o.as<bf16>(), sh, st);
+            KVP_CUDA(cudaEventRecord(e1, st));
+            KVP_CUDA(cudaEventSynchronize(e1));
+            float x = 0;
+            KVP_CUDA(cudaEventElapsedTime(&x, e0, e1));
+            if (i) t.push_back(x);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        std::sort(t.begin(), t.end());
+        *ms = t[t.size() / 2];
+    });
+}
+
 kvp_status kvp_rank_begin(kvp_engine* e, const float* rows, int64_t n_rows, int64_t start, int64_t held,
                           int32_t rows_on_device, void* const* kv_bufs) {
     return guard([&] {

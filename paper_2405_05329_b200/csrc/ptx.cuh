@@ -50,9 +50,32 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
     return ok != 0;
 }
 
+// non-blocking probe (test_wait never suspends the thread)
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+// Blocking wait with a watchdog: a phase that never completes (a lost arrival) traps after
+// 2^26 failed probes (each try_wait suspends for a while; > 0.1 s in all) instead of
+// hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef KVP_WATCHDOG
+    uint32_t n = 0;
+    while (!mbar_try_wait(bar, parity)) {
+        if (++n == (1u << 26)) __trap();
+    }
+#else
     while (!mbar_try_wait(bar, parity)) {
     }
+#endif
 }
 
 // ----------------------------------------------------------------------- TMA

@@ -48,8 +48,11 @@ class Transport:
     def _staged(self, t) -> bool:
         return self.backend == "gloo" and t.is_cuda
 
-    def exchange(self, sends, recvs):
-        """sends: [(tensor, dst)], recvs: [(tensor, src)] -- one batched group."""
+    def exchange(self, sends, recvs, wait: bool = True):
+        """sends: [(tensor, dst)], recvs: [(tensor, src)] -- one batched group.  wait=False
+        (sends only) returns the pending works instead of joining them: with NCCL the
+        transfer then runs on the communicator's own stream, overlapping the caller's later
+        kernels; the caller joins the works (and keeps the tensors alive) before reuse."""
         import torch
         dist = self.dist
         staged_recv = []
@@ -65,11 +68,16 @@ class Transport:
                 staged_recv.append((host, t))
                 t = host
             ops.append(dist.P2POp(dist.irecv, t, src, self.group))
-        if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
+        works = dist.batch_isend_irecv(ops) if ops else []
+        if not wait:
+            if recvs:
+                raise ValueError("deferred exchange is for sends only")
+            return works
+        for w in works:
+            w.wait()
         for host, dev in staged_recv:
             dev.copy_(host, non_blocking=False)
+        return []
 
 
 # ------------------------------------------------------------------ executors
@@ -210,6 +218,7 @@ def run_rank(strategy: kv.Strategy, rows, partition: kv.ContextPartition, execut
     inbound = []  # (header tensor, kind, layer, expected start, expected end)
     out_links = collections.defaultdict(_Link)
     sent_ctr = [0]
+    in_flight = []  # KVR handoff sends still on the wire (joined before the rank's result)
     for layer in range(n_layers):
         executor.qkv(layer)
         K, V = executor.kv(layer)
@@ -227,9 +236,12 @@ def run_rank(strategy: kv.Strategy, rows, partition: kv.ContextPartition, execut
                     _apply_fault(fault, rank, _header(KIND_HANDOFF, layer, rank, 0, stop), link, sent_ctr)
                     msg = link.outbox.popleft() if link.outbox else _header(KIND_CLOSED, layer, rank, 0, stop)
                     sends += [(executor.header(msg), rank + 1), (K[:stop], rank + 1), (V[:stop], rank + 1)]
-                # the receive must land before the cumulative cache is forwarded
+                # the receive must land before the cumulative cache is forwarded (and before
+                # this layer's attention); the send is NOT joined here: layer l's K/V buffers
+                # are never written again, so its transfer to rank i+1 overlaps this rank's
+                # attention/FFN of layer l and the layers after it
                 transport.exchange([], recvs)
-                transport.exchange(sends, [])
+                in_flight.append((transport.exchange(sends, [], wait=False), sends))  # keeps the tensors alive
                 k_rows = stop
             elif strategy == kv.Strategy.TSP:
                 sends, recvs = [], []
@@ -254,6 +266,10 @@ def run_rank(strategy: kv.Strategy, rows, partition: kv.ContextPartition, execut
                 k_rows = C_
         dots += c * k_rows
         executor.finish(layer, k_rows)
+    with executor.stream():
+        for works, _ in in_flight:
+            for w in works:
+                w.wait()
     hidden, ms = executor.end()
     sent = sent_ctr[0]
 

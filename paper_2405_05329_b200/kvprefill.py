@@ -114,6 +114,8 @@ _SIGS = {
     "kvp_engine_kernel_stats": (C.c_int, [_P, C.POINTER(_KStats), C.c_int32, C.POINTER(C.c_int32)]),
     "kvp_engine_profile_layer": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, C.POINTER(C.c_float),
                                            C.POINTER(C.c_float)]),
+    "kvp_bench_attn": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                 C.POINTER(C.c_float)]),
     "kvp_bench_gemm": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_float),
                                  C.POINTER(C.c_int32)]),
     "kvp_rank_begin": (C.c_int, [_P, _P, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.POINTER(C.c_void_p)]),
@@ -420,6 +422,14 @@ class WeightSet:
         ms, bn = C.c_float(), C.c_int32()
         _check(lib().kvp_bench_gemm(self._h, M, N, K, epi, reps, C.byref(ms), C.byref(bn)), "bench_gemm")
         return float(ms.value), 2.0 * M * N * K / (ms.value * 1e-3) / 1e12, int(bn.value)
+
+    def bench_attn(self, q_rows: int, offset: int, n_heads: int, n_kv_heads: int, head_dim: int, reps: int = 10):
+        """Median device ms of the bf16 attention kernel alone and its causal-visible TFLOP/s."""
+        ms = C.c_float()
+        _check(lib().kvp_bench_attn(self._h, q_rows, offset, n_heads, n_kv_heads, head_dim, reps, C.byref(ms)),
+               "bench_attn")
+        pairs = q_rows * offset + q_rows * (q_rows + 1) / 2
+        return ms.value, 4.0 * head_dim * n_heads * pairs / (ms.value * 1e-3) / 1e12
 
     def last_launch_count(self) -> int:
         v = C.c_int64()
