@@ -19,6 +19,8 @@ KEYS = {
     "dram_throughput_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
     "sm_throughput_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "smem_tc_wavefronts_pct": "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "xu_mufu_pipe_pct_active": "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "registers": "launch__registers_per_thread",
     "grid": "launch__grid_size",
     "block": "launch__block_size",
