@@ -15,6 +15,9 @@ shapes = {  # name: (M, N, K, epi)
     "sq8192": (8192, 8192, 8192, 3),
     "l16_qkv": (16384, 12288, 4096, 0), "l16_o": (16384, 4096, 4096, 1), "l16_ffn1": (16384, 8192, 4096, 2),
     "l16_ffn2": (16384, 4096, 8192, 1),
+    "p4_qkv": (1024, 12288, 4096, 0), "p4_o": (1024, 4096, 4096, 1), "p4_ffn1": (1024, 8192, 4096, 2),
+    "p4_ffn2": (1024, 4096, 8192, 1), "p2_qkv": (2048, 12288, 4096, 0), "p2_o": (2048, 4096, 4096, 1),
+    "p2_ffn1": (2048, 8192, 4096, 2), "p2_ffn2": (2048, 4096, 8192, 1),
 }
 only = set(sys.argv[1:])
 out = {}
