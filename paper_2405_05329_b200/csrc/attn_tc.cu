@@ -186,6 +186,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // PDL: prologue overlapped with the previous kernel's tail; wait before touching its outputs
+    ptx::griddep_launch_dependents();
+    ptx::griddep_wait();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -448,7 +451,17 @@ void launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShap
     }
     dim3 grid(static_cast<unsigned>(sh.n_heads), static_cast<unsigned>((sh.q_rows + 2 * BQ - 1) / (2 * BQ)));
     note_launch();
-    attn_tc_kernel<HD, NPOLY><<<grid, THREADS, ACfg<HD>::SMEM, s>>>(tq, tk, tv, a);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = ACfg<HD>::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, attn_tc_kernel<HD, NPOLY>, tq, tk, tv, a);
     if (a.trace) {
         uint32_t host[16 * 512];
         cudaMemcpyAsync(host, a.trace, sizeof(host), cudaMemcpyDeviceToHost, s);

@@ -42,6 +42,13 @@ void set_last_error(const std::string& msg) { t_last_error = msg; }
 static std::atomic<int64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 int64_t launch_count() { return g_launches.load(); }
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("KVP_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 // rng.hpp:10-37 (host side: only the stream seeds are derived here)
 static uint64_t splitmix_next(uint64_t& s) {

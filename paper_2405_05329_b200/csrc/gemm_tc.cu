@@ -356,6 +356,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     if constexpr (NCTA == 2) ptx::cluster_sync();  // peer barriers initialised before any remote use
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // PDL: the prologue above overlapped the previous kernel's tail; no global memory is
+    // touched before the previous grid has completed
+    ptx::griddep_launch_dependents();
+    ptx::griddep_wait();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -556,13 +560,15 @@ void launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& 
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = Cf::smem_for(KIND);
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = NCTA;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     cudaLaunchKernelEx(&cfg, kern, ta, tb, tbh, M, N, K, n_full, group_m, ep);
 }
 

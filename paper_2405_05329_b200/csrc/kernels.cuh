@@ -14,6 +14,8 @@ using bf16 = __nv_bfloat16;
 // Counts every kernel launch issued by this library (the bench's gpu_launches claim).
 void note_launch();
 int64_t launch_count();
+// Programmatic dependent launch for the tcgen05 kernels (KVP_PDL=0 disables).
+bool pdl_enabled();
 
 // ---------------------------------------------------------------- weights.cu
 // Fills a rows x cols matrix from init_weights' SplitMix64 stream (weights.hpp:41-47),

@@ -78,6 +78,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// ------------------------------------------------- programmatic dependent launch
+// Let the next kernel in the stream (launched with programmatic stream serialization) start
+// its prologue on SMs this grid frees; it blocks in griddep_wait() until this grid completes.
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+// Block until the preceding grid (programmatic dependency) has completed and its memory is
+// visible; returns at once when there is none.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ----------------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
