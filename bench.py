@@ -210,6 +210,40 @@ def run_reference_arm(args, w, rank, world):
 
 
 # ------------------------------------------------------------------ our arm
+def kv_handoff_bandwidth(b, w, rank, world, local, reps=10):
+    """GB/s of the busiest KV-Runahead link (rank p-2 -> p-1 carries K and V rows [0, b_{p-1})
+    per layer) measured in isolation with NCCL send/recv, against 900 GB/s per direction of
+    NVLink 5.  Device time between CUDA events around each transfer (on the receiver)."""
+    import torch
+    import torch.distributed as dist
+    kv_dim = w["n_kv_heads"] * (w["d_model"] // w["n_heads"])
+    rows = b[world - 1]
+    nbytes = 2 * rows * kv_dim * 2  # K and V, bf16
+    src, dst = world - 2, world - 1
+    buf = torch.empty(nbytes // 2, dtype=torch.bfloat16, device=f"cuda:{local}")
+    times = []
+    for i in range(reps + 2):
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        if rank == src:
+            dist.send(buf, dst)
+        elif rank == dst:
+            dist.recv(buf, src)
+        e1.record()
+        torch.cuda.synchronize()
+        if i >= 2 and rank == dst:
+            times.append(e0.elapsed_time(e1))
+    out = [None]
+    if rank == dst:
+        ms = statistics.median(times)
+        out = [{"link": f"{src}->{dst}", "bytes_per_layer": nbytes, "ms": ms, "gbs": nbytes / (ms * 1e-3) / 1e9,
+                "peak_gbs": 900.0, "frac": nbytes / (ms * 1e-3) / 1e9 / 900.0,
+                "note": "busiest link, isolated NCCL send/recv; in the prefill it overlaps compute"}]
+    dist.broadcast_object_list(out, src=dst)
+    return out[0]
+
+
 def run_multi(args, w, rank, world, local):
     """One process per GPU: KVR chain / TSP all-gather over NCCL through the distributed driver."""
     import torch
@@ -254,15 +288,24 @@ def run_multi(args, w, rank, world, local):
         step(rows_dev)
     dist.barrier()
     torch.cuda.synchronize()
-    times = []
+    times, launches = [], 0
     with ClockSampler(local) as clk:
         t0 = time.perf_counter()
         for _ in range(args.steps):
             times.append(step(rows_dev).ttft_ms)
+            launches += W.last_launch_count()
         torch.cuda.synchronize()
         dist.barrier()
         wall = time.perf_counter() - t0
     ms = statistics.mean(times)
+    all_launches = [None] * world
+    dist.all_gather_object(all_launches, launches)
+    handoff = None
+    if strategy == kv.Strategy.KVR and world > 1:
+        try:
+            handoff = kv_handoff_bandwidth(b, w, rank, world, local)
+        except Exception as ex:  # the measurement must never break the bench line
+            handoff = {"error": str(ex)}
     W.set_profiling(True)
     step(rows_dev)
     stats = W.kernel_stats()
@@ -296,7 +339,8 @@ def run_multi(args, w, rank, world, local):
                              "frac": achieved / peaks["bf16_sustained"], "traffic": None},
                 "kernels_rank0": {k: {"launches": v["launches"], "ms": round(v["total_ms"], 4)} for k, v in stats.items()},
                 "clocks": clocks[0], "clocks_all": clocks,
-                "gpu_launches": None,
+                "gpu_launches": sum(all_launches),
+                "kv_handoff": handoff,
                 "e2e": {"value": statistics.mean(e2e_t), "unit": "ms", "h2d_bytes_per_step": C * w["d_model"] * 4,
                         "d2h_bytes_per_step": C * w["d_model"] * 4} if e2e_t else None}
         print(json.dumps(line), flush=True)

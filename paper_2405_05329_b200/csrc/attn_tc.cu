@@ -33,9 +33,10 @@ bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t 
 
 namespace {
 
-constexpr int BQ = 128;   // queries per tile (two tiles per CTA)
-constexpr int BKV = 128;  // keys per tile
-constexpr int THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 softmax
+constexpr int BQ = 128;  // queries per tile (NT tiles per CTA)
+// warp 0 TMA, warp 1 MMA, warps 2 .. 2+4*NT-1 softmax (four per query tile)
+template <int NT>
+constexpr int threads_for() { return 64 + NT * 128; }
 constexpr uint32_t TMEM_COLS = 512;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units: p <= 2^8 between rescales
 constexpr int DEFAULT_POLY_128 = 0;        // exp2 column pairs (of 16) on the FMA pipe
@@ -43,15 +44,20 @@ constexpr int DEFAULT_POLY_64 = 0;
 
 // K and V tiles have separate smem rings: K(j) is released as soon as both S MMAs of key
 // tile j are done, so K(j+1..) streams in while the softmax of tile j runs.
-template <int HD>
+// NT query tiles of BQ rows per CTA, BKV-key tiles.  TMEM: S_x (fp32, BKV columns, P packed
+// over its first BKV/2) at x*BKV, O_x (HD columns) at NT*BKV + x*HD.
+template <int HD, int NT, int BKV>
 struct ACfg {
+    static_assert(NT * (BKV + HD) <= 512, "TMEM holds NT x (S + O)");
+    static_assert(BKV % 32 == 0 && BKV <= 128, "key tile");
     static constexpr int HALVES = HD / 64;  // 64-wide (128 B) TMA boxes
+    static constexpr uint32_t O_BASE = NT * BKV;
     static constexpr uint32_t Q_BYTES = BQ * HD * 2;
     static constexpr uint32_t KV_BYTES = BKV * HD * 2;
     static constexpr int KST = HD == 64 ? 4 : 3;  // K stages
     static constexpr int VST = HD == 64 ? 3 : 2;  // V stages
     static constexpr uint32_t XCH = 0;
-    static constexpr uint32_t NEED = 2 * Q_BYTES + (KST + VST) * KV_BYTES + 256 + XCH;
+    static constexpr uint32_t NEED = NT * Q_BYTES + (KST + VST) * KV_BYTES + 256 + XCH;
     // + up to 1 KB of slack for aligning the dynamic smem base to 1024 B (the SW128 atoms)
     static constexpr uint32_t SMEM = NEED + 1024 <= 232448 ? NEED + 1024 : 232448;
     static_assert(NEED + 512 <= 232448, "attention smem over the 227 KB opt-in limit");
@@ -120,11 +126,11 @@ struct AttnArgs {
             a.trace[(ev) * 512 + (j)] = static_cast<uint32_t>(clock());                                \
     } while (0)
 
-template <int HD, int NPOLY>
-__global__ void __launch_bounds__(THREADS, 1)
+template <int HD, int NT, int BKV, int NPOLY>
+__global__ void __launch_bounds__(threads_for<NT>(), 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
-    using C = ACfg<HD>;
+    using C = ACfg<HD, NT, BKV>;
     constexpr int KST = C::KST, VST = C::VST;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment by pointer arithmetic on the __shared__ array, so the compiler keeps
@@ -132,8 +138,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t pad = (1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u;
     if (pad + C::NEED > C::SMEM) __trap();  // dynamic smem base too far from 1 KB alignment
     uint8_t* smem = smem_raw + pad;
-    uint8_t* sQ = smem;                  // [2] query tiles
-    uint8_t* sK = sQ + 2 * C::Q_BYTES;     // [KST] stages
+    uint8_t* sQ = smem;                    // [NT] query tiles
+    uint8_t* sK = sQ + NT * C::Q_BYTES;    // [KST] stages
     uint8_t* sV = sK + KST * C::KV_BYTES;  // [VST] stages
     uint64_t* bar = reinterpret_cast<uint64_t*>(sV + VST * C::KV_BYTES);
     uint64_t* q_full = bar;
@@ -141,25 +147,28 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* k_empty = k_full + KST;        // [KST]
     uint64_t* v_full = k_empty + KST;        // [VST]
     uint64_t* v_empty = v_full + VST;        // [VST]
-    uint64_t* s_full = v_empty + VST;        // [2] query tiles
-    uint64_t* p_full = s_full + 2;           // [2] query tiles
-    uint64_t* o_done = p_full + 2;           // [2] query tiles
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+    uint64_t* s_full = v_empty + VST;        // [NT] query tiles
+    uint64_t* p_full = s_full + NT;          // [NT] query tiles
+    uint64_t* o_done = p_full + NT;          // [NT] query tiles
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + NT);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int num_pairs = static_cast<int>((a.q_rows + 2 * BQ - 1) / (2 * BQ));
-    // grid = (heads, pairs): the block scheduler walks x fastest, so ALL heads of the heaviest
-    // (latest) query pair are dispatched first -- a global longest-first order over the causal
-    // work imbalance
-    const int pair = num_pairs - 1 - static_cast<int>(blockIdx.y);
+    const int num_groups = static_cast<int>((a.q_rows + NT * BQ - 1) / (NT * BQ));
+    // grid = (heads, query groups): the block scheduler walks x fastest, so ALL heads of the
+    // heaviest (latest) query group are dispatched first -- a global longest-first order over
+    // the causal work imbalance
+    const int grp = num_groups - 1 - static_cast<int>(blockIdx.y);
     const int h = blockIdx.x;
     const int g = h / a.group;
-    const int64_t q0 = static_cast<int64_t>(pair) * 2 * BQ;
-    // key tiles needed by each query tile (tile b covers tile a's range plus one)
-    const int64_t last_a = (q0 + BQ - 1 < a.q_rows - 1) ? q0 + BQ - 1 : a.q_rows - 1;
-    const int64_t last_b = (q0 + 2 * BQ - 1 < a.q_rows - 1) ? q0 + 2 * BQ - 1 : a.q_rows - 1;
-    const int n_kt[2] = {static_cast<int>((a.offset + last_a) / BKV) + 1,
-                         static_cast<int>((a.offset + (last_b > last_a ? last_b : last_a)) / BKV) + 1};
+    const int64_t q0 = static_cast<int64_t>(grp) * NT * BQ;
+    // key tiles needed by each query tile (non-decreasing: the last tile reads every K/V tile)
+    int n_kt[NT];
+#pragma unroll
+    for (int x = 0; x < NT; ++x) {
+        const int64_t last = (q0 + (x + 1) * BQ - 1 < a.q_rows - 1) ? q0 + (x + 1) * BQ - 1 : a.q_rows - 1;
+        n_kt[x] = static_cast<int>((a.offset + last) / BKV) + 1;
+        if (x > 0 && n_kt[x] < n_kt[x - 1]) n_kt[x] = n_kt[x - 1];
+    }
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmQ);
@@ -174,7 +183,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             ptx::mbar_init(&v_full[s], 1);
             ptx::mbar_init(&v_empty[s], 1);
         }
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < NT; ++s) {
             ptx::mbar_init(&s_full[s], 1);
             ptx::mbar_init(&p_full[s], 4);  // the 4 softmax warps of the tile
             ptx::mbar_init(&o_done[s], 1);
@@ -192,15 +201,15 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            ptx::mbar_arrive_expect_tx(q_full, 2 * C::Q_BYTES);
-            for (int x = 0; x < 2; ++x)
+            ptx::mbar_arrive_expect_tx(q_full, NT * C::Q_BYTES);
+            for (int x = 0; x < NT; ++x)
                 for (int hv = 0; hv < C::HALVES; ++hv)
                     ptx::tma_load_2d(sQ + x * C::Q_BYTES + hv * BQ * 128, &tmQ, q_full, h * HD + hv * 64,
                                      static_cast<int32_t>(q0 + x * BQ));
-            // K(t), V(t) in need order; K(t) waits for both S MMAs of tile t - KST, V(t) for both
-            // PV MMAs of tile t - VST, so K runs a stage further ahead (blocking waits: the
-            // producer lane never spins on the issue slots of the softmax warps of its SMSP)
-            for (int t = 0; t < n_kt[1]; ++t) {
+            // K(t), V(t) in need order; K(t) waits for the S MMAs of key tile t - KST, V(t) for
+            // its PV MMAs, so K runs a stage further ahead (blocking waits: the producer lane
+            // never spins on the issue slots of the softmax warps of its SMSP)
+            for (int t = 0; t < n_kt[NT - 1]; ++t) {
                 const int sk = t % KST, sv = t % VST;
                 ptx::mbar_wait(&k_empty[sk], ((t / KST) & 1) ^ 1);
                 ATTN_TRACE(12, t);
@@ -224,7 +233,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const int s = t % KST;
                 ptx::mbar_wait(&k_full[s], (t / KST) & 1);
                 ptx::tc_fence_after();
-                ATTN_TRACE(0 + x, t);
+                if (x < 2) ATTN_TRACE(0 + x, t);
                 const uint32_t q_addr = ptx::smem_u32(sQ + x * C::Q_BYTES);
                 const uint32_t k_addr = ptx::smem_u32(sK + s * C::KV_BYTES);
 #pragma unroll
@@ -232,52 +241,48 @@ __global__ void __launch_bounds__(THREADS, 1)
                     const uint32_t off = (k >> 2) * (BQ * 128) + (k & 3) * 32;
                     const uint64_t ad = ptx::smem_desc_sw128(q_addr + off, 16, 1024);
                     const uint64_t bd = ptx::smem_desc_sw128(k_addr + (k >> 2) * (BKV * 128) + (k & 3) * 32, 16, 1024);
-                    ptx::mma_bf16_ss(tmem + x * 128, ad, bd, idesc_s, k != 0);
+                    ptx::mma_bf16_ss(tmem + x * BKV, ad, bd, idesc_s, k != 0);
                 }
                 ptx::mma_commit(&s_full[x]);
-                if (x == 1) ptx::mma_commit(&k_empty[s]);  // tile b is the last reader of K(t)
+                if (x == NT - 1) ptx::mma_commit(&k_empty[s]);  // the last tile is the last reader of K(t)
             };
             auto issue_pv = [&](int x, int t) {
                 const int s = t % VST;
                 ptx::mbar_wait(&p_full[x], t & 1);
                 ptx::mbar_wait(&v_full[s], (t / VST) & 1);
                 ptx::tc_fence_after();
-                ATTN_TRACE(2 + x, t);
+                if (x < 2) ATTN_TRACE(2 + x, t);
                 const uint32_t v_addr = ptx::smem_u32(sV + s * C::KV_BYTES);
 #pragma unroll
                 for (int k = 0; k < BKV / 16; ++k) {
                     // B = V[keys 16k..16k+15][hd]: MN-major SW128, LBO = next 64-wide hd block,
                     // SBO = next 8 keys.
                     const uint64_t bd = ptx::smem_desc_sw128(v_addr + k * 16 * 128, BKV * 128, 1024);
-                    ptx::mma_bf16_ts(tmem + 256 + x * 128, tmem + x * 128 + k * 8, bd, idesc_o, (t | k) != 0);
+                    ptx::mma_bf16_ts(tmem + C::O_BASE + x * HD, tmem + x * BKV + k * 8, bd, idesc_o, (t | k) != 0);
                 }
                 ptx::mma_commit(&o_done[x]);
-                if (x == 1) ptx::mma_commit(&v_empty[s]);  // tile b is the last reader of V(t)
+                if (x == NT - 1) ptx::mma_commit(&v_empty[s]);  // the last tile is the last reader of V(t)
             };
             ptx::mbar_wait(q_full, 0);
-            issue_s(0, 0);
-            issue_s(1, 0);
-            for (int j = 0; j < n_kt[1]; ++j) {
-                if (j < n_kt[0]) {
-                    issue_pv(0, j);
-                    if (j + 1 < n_kt[0]) {
-                        // S_a(j+1) overwrites the TMEM columns P_a(j) is read from: tcgen05.mma
-                        // ops of one thread execute in issue order, so waiting for PV_a(j) is
+            for (int x = 0; x < NT; ++x) issue_s(x, 0);
+            for (int j = 0; j < n_kt[NT - 1]; ++j) {
+#pragma unroll
+                for (int x = 0; x < NT; ++x) {
+                    if (j >= n_kt[x]) continue;
+                    issue_pv(x, j);
+                    if (j + 1 < n_kt[x]) {
+                        // S_x(j+1) overwrites the TMEM columns P_x(j) is read from: tcgen05.mma
+                        // ops of one thread execute in issue order, so waiting for PV_x(j) is
                         // only needed when the pipeline is not trusted (a.mma_wait)
-                        if (a.mma_wait) ptx::mbar_wait(&o_done[0], j & 1);
-                        issue_s(0, j + 1);
+                        if (a.mma_wait) ptx::mbar_wait(&o_done[x], j & 1);
+                        issue_s(x, j + 1);
                     }
-                }
-                issue_pv(1, j);
-                if (j + 1 < n_kt[1]) {
-                    if (a.mma_wait) ptx::mbar_wait(&o_done[1], j & 1);
-                    issue_s(1, j + 1);
                 }
             }
         }
     } else {
-        // 8 softmax warps: warps 2..5 own tile a, warps 6..9 tile b; warp w reads TMEM lane
-        // quarter w % 4, one thread per query row (all 128 keys of the tile, no exchange).
+        // 4*NT softmax warps: warps 2+4x .. 5+4x own query tile x; warp w reads TMEM lane
+        // quarter w % 4, one thread per query row (all BKV keys of the tile, no exchange).
         const int x = (warp - 2) >> 2;                         // query tile
         const uint32_t quarter = warp & 3;                     // TMEM lane quarter this warp may access
         const int xrow = static_cast<int>(quarter) * 32 + lane;
@@ -288,8 +293,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int nt = n_kt[x];
         const float2 sl2v = make_float2(a.sl2, a.sl2);
         float m_run = -INFINITY, l = 0.f;
-        // exp2 of the row's 128 scores against base m (log2 units), P -> TMEM as packed bf16
-        // over the first 64 S columns; returns the row sum of P
+        // exp2 of the row's BKV scores against base m (log2 units), P -> TMEM as packed bf16
+        // over the first BKV/2 S columns; returns the row sum of P
         auto exp_store = [&](const float (&sv)[BKV], float m, bool diag) -> float {
             const float2 nb2 = make_float2(-m, -m);
             float2 lacc = make_float2(0.f, 0.f);
@@ -315,20 +320,20 @@ __global__ void __launch_bounds__(THREADS, 1)
                     lacc = fadd2(lacc, pv);
                     pk[i] = ptx::pack_bf16(pv.x, pv.y);
                 }
-                ptx::tmem_st16(lane_base + x * 128 + c * 16, pk);
+                ptx::tmem_st16(lane_base + x * BKV + c * 16, pk);
             }
             return lacc.x + lacc.y;
         };
         for (int j = 0; j < nt; ++j) {
             ptx::mbar_wait(&s_full[x], j & 1);
             ptx::tc_fence_after();
-            const bool tr = quarter == 0 && lane == 0;
+            const bool tr = quarter == 0 && lane == 0 && x < 2;
             if (tr) ATTN_TRACE(4 + x, j);
             float sv[BKV];
             {
                 uint32_t r[BKV / 32][32];
 #pragma unroll
-                for (int c = 0; c < BKV / 32; ++c) ptx::tmem_ld32(lane_base + x * 128 + c * 32, r[c]);
+                for (int c = 0; c < BKV / 32; ++c) ptx::tmem_ld32(lane_base + x * BKV + c * 32, r[c]);
                 ptx::tmem_ld_wait();
 #pragma unroll
                 for (int c = 0; c < BKV / 32; ++c)
@@ -365,11 +370,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                     for (int c = 0; c < HD / 16; ++c) {
                         uint32_t r[16];
-                        ptx::tmem_ld16(lane_base + 256 + x * 128 + c * 16, r);
+                        ptx::tmem_ld16(lane_base + C::O_BASE + x * HD + c * 16, r);
                         ptx::tmem_ld_wait();
 #pragma unroll
                         for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-                        ptx::tmem_st16(lane_base + 256 + x * 128 + c * 16, r);
+                        ptx::tmem_st16(lane_base + C::O_BASE + x * HD + c * 16, r);
                     }
                     ptx::tmem_st_wait();
                 }
@@ -392,7 +397,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int c = 0; c < HD / 32; ++c) {
             uint32_t r[32];
-            ptx::tmem_ld32(lane_base + 256 + x * 128 + c * 32, r);
+            ptx::tmem_ld32(lane_base + C::O_BASE + x * HD + c * 32, r);
             ptx::tmem_ld_wait();
             if (row < a.q_rows) {
 #pragma unroll
@@ -423,7 +428,7 @@ int mma_wait_flag() {
     return w;
 }
 
-template <int HD, int NPOLY>
+template <int HD, int NT, int BKV, int NPOLY>
 void launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShape& sh, cudaStream_t s) {
     CUtensorMap tq, tk, tv;
     if (!make_tmap_bf16(&tq, Q, static_cast<uint64_t>(sh.n_heads) * HD, sh.q_rows, sh.ldq, 64, BQ) ||
@@ -434,8 +439,8 @@ void launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShap
     int dev = 0;
     cudaGetDevice(&dev);
     if (configured != dev) {
-        cudaFuncSetAttribute(attn_tc_kernel<HD, NPOLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             ACfg<HD>::SMEM);
+        cudaFuncSetAttribute(attn_tc_kernel<HD, NT, BKV, NPOLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             ACfg<HD, NT, BKV>::SMEM);
         configured = dev;
     }
     AttnArgs a{sh.q_rows, sh.k_rows, sh.offset, sh.n_heads, sh.n_heads / sh.n_kv_heads, sh.ldo, O,
@@ -449,19 +454,19 @@ void launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShap
         a.trace = buf;
         a.trace_blk = atoi(trace_env);
     }
-    dim3 grid(static_cast<unsigned>(sh.n_heads), static_cast<unsigned>((sh.q_rows + 2 * BQ - 1) / (2 * BQ)));
+    dim3 grid(static_cast<unsigned>(sh.n_heads), static_cast<unsigned>((sh.q_rows + NT * BQ - 1) / (NT * BQ)));
     note_launch();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
-    cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = ACfg<HD>::SMEM;
+    cfg.blockDim = dim3(threads_for<NT>());
+    cfg.dynamicSmemBytes = ACfg<HD, NT, BKV>::SMEM;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, attn_tc_kernel<HD, NPOLY>, tq, tk, tv, a);
+    cudaLaunchKernelEx(&cfg, attn_tc_kernel<HD, NT, BKV, NPOLY>, tq, tk, tv, a);
     if (a.trace) {
         uint32_t host[16 * 512];
         cudaMemcpyAsync(host, a.trace, sizeof(host), cudaMemcpyDeviceToHost, s);
@@ -474,12 +479,12 @@ void launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShap
     }
 }
 
-template <int HD>
+template <int HD, int NT, int BKV>
 void launch_poly(int np, const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShape& sh, cudaStream_t s) {
     switch (np) {
-        case 0: launch<HD, 0>(Q, K, V, O, sh, s); break;
-        case 2: launch<HD, 2>(Q, K, V, O, sh, s); break;
-        case 4: launch<HD, 4>(Q, K, V, O, sh, s); break;
+        case 0: launch<HD, NT, BKV, 0>(Q, K, V, O, sh, s); break;
+        case 2: launch<HD, NT, BKV, 2>(Q, K, V, O, sh, s); break;
+        case 4: launch<HD, NT, BKV, 4>(Q, K, V, O, sh, s); break;
         default: throw std::runtime_error("attn_tc: KVP_ATTN_POLY must be 0, 2 or 4");
     }
 }
@@ -496,10 +501,22 @@ void attn_bf16_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const At
         return e ? atoi(e) : -1;
     }();
     if (sh.head_dim != 128 && sh.head_dim != 64) throw std::runtime_error("attn_tc: head_dim must be 64 or 128");
-    if (sh.offset + sh.q_rows + BKV >= (int64_t(1) << 31)) throw std::runtime_error("attn_tc: positions must be < 2^31");
+    if (sh.offset + sh.q_rows + 128 >= (int64_t(1) << 31)) throw std::runtime_error("attn_tc: positions must be < 2^31");
+    // hd 64: two query tiles x 128-key tiles; KVP_ATTN_HD64_TILES=3 selects three query tiles x
+    // 96-key tiles (TMEM 3 x (96 + 64) columns, three softmax warps per SMSP's MUFU) -- measured
+    // no faster: the in-order MMA issuer then waits ~1200 clk per tile for its turn
+    static const int hd64_tiles = [] {
+        const char* e = getenv("KVP_ATTN_HD64_TILES");
+        return e ? atoi(e) : 2;
+    }();
     const bool h128 = sh.head_dim == 128;
     const int np = poly >= 0 ? poly : (h128 ? DEFAULT_POLY_128 : DEFAULT_POLY_64);
-    h128 ? launch_poly<128>(np, Q, K, V, O, sh, s) : launch_poly<64>(np, Q, K, V, O, sh, s);
+    if (h128)
+        launch_poly<128, 2, 128>(np, Q, K, V, O, sh, s);
+    else if (hd64_tiles == 2)
+        launch_poly<64, 2, 128>(np, Q, K, V, O, sh, s);
+    else
+        launch_poly<64, 3, 96>(np, Q, K, V, O, sh, s);
 }
 
 }  // namespace kvp

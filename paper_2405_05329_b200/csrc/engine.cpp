@@ -593,7 +593,7 @@ struct kvp_engine {
     bool profiling = false;
     // multi-process rank session
     bool in_session = false;
-    int64_t sess_rows = 0, sess_start = 0;
+    int64_t sess_rows = 0, sess_start = 0, sess_launch0 = 0;
 };
 
 namespace kvp {
@@ -1250,6 +1250,7 @@ kvp_status kvp_rank_begin(kvp_engine* e, const float* rows, int64_t n_rows, int6
         e->in_session = true;
         e->sess_rows = n_rows;
         e->sess_start = start;
+        e->sess_launch0 = launch_count();
         e->last_p = 1;
     });
 }
@@ -1326,6 +1327,7 @@ kvp_status kvp_rank_end(kvp_engine* e, float* out_rows, int32_t out_on_device, f
         KVP_CUDA(cudaEventElapsedTime(&t, R.ev_begin, R.ev_done));
         if (ms) *ms = t;
         e->last_ttft = t;
+        e->last_launches = launch_count() - e->sess_launch0;  // this rank's kernels of the session
         e->in_session = false;
     });
 }
