@@ -188,6 +188,29 @@ kvp_status kvp_rank_finish(kvp_engine* e, int64_t layer, int64_t k_rows);
  * nullable) and the last local row (d floats, host, nullable); *ms = device time of the rank
  * from kvp_rank_begin to the last layer (nullable). */
 kvp_status kvp_rank_end(kvp_engine* e, float* out_rows, int32_t out_on_device, float* last_row, float* ms);
+/* Switch the open session to the decode kernels (bf16: HBM-bound GEMV + split-key attention;
+ * at most 8 rows).  f32 engines keep the ordered SIMT kernels.  New (no reference
+ * counterpart). */
+kvp_status kvp_rank_set_decode(kvp_engine* e, int32_t on);
+
+/* ------------------------------------------- KV cache + decode */
+/* The reference stops at the first token (engine.hpp:88); its natural consumer is a decode
+ * step on the last rank's full KV cache.  A kvp_kv_cache owns per-layer K/V
+ * device buffers of `capacity` rows; kvp_prefill_cached runs the single-rank prompt phase
+ * into it (length := C; hidden_out C x d and first_token_hidden d floats are host, nullable)
+ * and kvp_decode appends n_rows (<= 8) new rows at positions [length, length + n_rows)
+ * attending to the whole cache (layer_qkv + layer_finish with offset = length), returning
+ * their final hidden rows (host, n_rows x d). */
+typedef struct kvp_kv_cache kvp_kv_cache;
+kvp_status kvp_kv_cache_create(kvp_engine* e, int64_t capacity, kvp_kv_cache** out);
+kvp_status kvp_kv_cache_destroy(kvp_kv_cache* c);
+kvp_status kvp_kv_cache_length(const kvp_kv_cache* c, int64_t* length);
+/* Truncate to `length` rows (e.g. to re-decode from an earlier position). */
+kvp_status kvp_kv_cache_reset(kvp_kv_cache* c, int64_t length);
+kvp_status kvp_prefill_cached(kvp_engine* e, kvp_kv_cache* c, const float* context, int64_t C, float* hidden_out,
+                              float* first_token_hidden, float* ms);
+kvp_status kvp_decode(kvp_engine* e, kvp_kv_cache* c, const float* rows, int64_t n_rows, float* out_rows,
+                      float* ms);
 
 /* ------------------------------------------- per-rank layer executor pieces */
 /* layer_qkv (model.hpp:189-192): hidden rows x d -> Q rows x q, K/V rows x kv. */

@@ -338,6 +338,8 @@ struct RankCtx {
     DevBuf h, h1, x, q, a, mid, kv, ssq;
     int64_t held = 0;  // rows per layer K (and V) buffer
     std::vector<void*> ext_kv;  // caller-owned per-layer K/V buffers (multi-process mode)
+    bool decode = false;        // decode step: HBM-bound GEMV + split-key attention kernels
+    DevBuf scratch;             // decode attention partials
     std::vector<cudaEvent_t> ev_send, ev_ready, t_start, t_qkv, t_attn, t_end;
     cudaEvent_t ev_begin = nullptr, ev_done = nullptr;
     // profiling: (class, flops, bytes, start event, end event) per launch
@@ -472,7 +474,12 @@ static void exec_qkv(const Shape& s, const LayerW& w, RankCtx& R, int64_t c, voi
             ep.ssq_parts = ssq_parts_for(s.d);
             ep.norm_cols = s.d;
         }
-        R.timed(K_GEMM_QKV, gf, 0, [&] { gemm_bf16_tc(R.x.as<bf16>(), c, s.d, w.wqkv_t, s.q + 2 * s.kv, ep, R.comp); });
+        R.timed(K_GEMM_QKV, gf, 0, [&] {
+            if (R.decode)
+                gemv_bf16(R.x.as<bf16>(), c, s.d, w.wqkv_t, s.q + 2 * s.kv, ep, R.comp);
+            else
+                gemm_bf16_tc(R.x.as<bf16>(), c, s.d, w.wqkv_t, s.q + 2 * s.kv, ep, R.comp);
+        });
     } else {
         const float* x = R.h.as<float>();
         if (s.rms) {
@@ -506,7 +513,11 @@ static void exec_finish(const Shape& s, const LayerW& w, RankCtx& R, int64_t c, 
     const double af = 4.0 * s.hd * s.h * pairs;
     if (s.prec == KVP_BF16) {
         R.timed(K_ATTN, af, 0, [&] {
-            if (attn_bf16_supported(sh.head_dim))
+            if (R.decode && (sh.head_dim == 64 || sh.head_dim == 128)) {
+                R.scratch.ensure(static_cast<size_t>(attn_decode_scratch_floats(sh)) * 4, R.device);
+                attn_decode_bf16(R.q.as<bf16>(), static_cast<const bf16*>(K), static_cast<const bf16*>(V), R.a.as<bf16>(),
+                                 sh, R.scratch.as<float>(), R.comp);
+            } else if (attn_bf16_supported(sh.head_dim))
                 attn_bf16(R.q.as<bf16>(), static_cast<const bf16*>(K), static_cast<const bf16*>(V), R.a.as<bf16>(), sh,
                           R.comp);
             else
@@ -525,7 +536,14 @@ static void exec_finish(const Shape& s, const LayerW& w, RankCtx& R, int64_t c, 
             e1.ssq_out = R.ssq.as<float>();
             e1.ssq_parts = ssq_parts_for(s.d);
         }
-        R.timed(K_GEMM_O, 2.0 * c * s.q * s.d, 0, [&] { gemm_bf16_tc(R.a.as<bf16>(), c, s.q, w.wo_t, s.d, e1, R.comp); });
+        // decode rows (R.decode) take the HBM-bound GEMV with the same epilogues
+        auto mm = [&](const bf16* A, int64_t K_, const bf16* B, int64_t N_, const GemmEpilogue& ep) {
+            if (R.decode)
+                gemv_bf16(A, c, K_, B, N_, ep, R.comp);
+            else
+                gemm_bf16_tc(A, c, K_, B, N_, ep, R.comp);
+        };
+        R.timed(K_GEMM_O, 2.0 * c * s.q * s.d, 0, [&] { mm(R.a.as<bf16>(), s.q, w.wo_t, s.d, e1); });
         GemmEpilogue e2;
         e2.kind = EPI_RELU;
         e2.out0 = R.mid.as<bf16>();
@@ -535,7 +553,7 @@ static void exec_finish(const Shape& s, const LayerW& w, RankCtx& R, int64_t c, 
             e2.ssq_parts = ssq_parts_for(s.d);
             e2.norm_cols = s.d;
         }
-        R.timed(K_GEMM_FFN1, 2.0 * c * s.d * s.f, 0, [&] { gemm_bf16_tc(R.x.as<bf16>(), c, s.d, w.w1_t, s.f, e2, R.comp); });
+        R.timed(K_GEMM_FFN1, 2.0 * c * s.d * s.f, 0, [&] { mm(R.x.as<bf16>(), s.d, w.w1_t, s.f, e2); });
         GemmEpilogue e3;
         e3.kind = EPI_RESID;
         e3.outf = R.h.as<float>();
@@ -548,7 +566,7 @@ static void exec_finish(const Shape& s, const LayerW& w, RankCtx& R, int64_t c, 
             e3.ssq_out = R.ssq.as<float>();
             e3.ssq_parts = ssq_parts_for(s.d);
         }
-        R.timed(K_GEMM_FFN2, 2.0 * c * s.f * s.d, 0, [&] { gemm_bf16_tc(R.mid.as<bf16>(), c, s.f, w.w2_t, s.d, e3, R.comp); });
+        R.timed(K_GEMM_FFN2, 2.0 * c * s.f * s.d, 0, [&] { mm(R.mid.as<bf16>(), s.f, w.w2_t, s.d, e3); });
     } else {
         R.timed(K_ATTN, af, 0, [&] {
             attn_simt_f32(R.q.as<float>(), static_cast<const float*>(K), static_cast<const float*>(V), R.a.as<float>(), sh,
@@ -1241,6 +1259,7 @@ kvp_status kvp_rank_begin(kvp_engine* e, const float* rows, int64_t n_rows, int6
         R.alloc(s, n_rows, held, kv_bufs == nullptr);
         if (kv_bufs) R.ext_kv.assign(kv_bufs, kv_bufs + 2 * s.L);
         R.profiling = e->profiling;
+        R.decode = false;
         R.marks.clear();
         R.pool_used = 0;
         KVP_CUDA(cudaSetDevice(R.device));
@@ -1266,6 +1285,15 @@ kvp_status kvp_rank_stream(kvp_engine* e, void** stream) {
     return guard([&] {
         std::lock_guard<std::mutex> g(e->mu);
         *stream = session_rank(e).comp;
+    });
+}
+
+kvp_status kvp_rank_set_decode(kvp_engine* e, int32_t on) {
+    return guard([&] {
+        std::lock_guard<std::mutex> g(e->mu);
+        RankCtx& R = session_rank(e);
+        if (on && e->sess_rows > 8) throw Error(KVP_ERR_INPUT, "decode steps take at most 8 new rows");
+        R.decode = on != 0 && e->s.prec == KVP_BF16;  // f32 keeps the ordered SIMT kernels
     });
 }
 
@@ -1430,3 +1458,86 @@ kvp_status kvp_layer_finish(kvp_engine* e, int64_t layer, const float* hidden, i
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ KV cache + decode (8f #4)
+struct kvp_kv_cache {
+    kvp_engine* e = nullptr;
+    kvp::DevBuf buf;
+    int64_t capacity = 0, length = 0;
+    std::vector<void*> ptrs;  // K_0, V_0, K_1, ...: [capacity x kv] each
+};
+
+kvp_status kvp_kv_cache_create(kvp_engine* e, int64_t capacity, kvp_kv_cache** out) {
+    return guard([&] {
+        if (!e || !out) throw Error(KVP_ERR_INPUT, "null argument");
+        if (capacity < 1) throw Error(KVP_ERR_CACHE, "cache capacity must be >= 1");
+        std::lock_guard<std::mutex> g(e->mu);
+        const Shape& s = e->s;
+        KVP_CUDA(cudaSetDevice(e->devices[0]));
+        auto c = std::make_unique<kvp_kv_cache>();
+        c->e = e;
+        c->capacity = capacity;
+        const size_t per = static_cast<size_t>(capacity) * s.kv * s.es();
+        c->buf.ensure(per * 2 * s.L, e->devices[0]);
+        for (int64_t i = 0; i < 2 * s.L; ++i) c->ptrs.push_back(c->buf.as<uint8_t>() + i * per);
+        *out = c.release();
+    });
+}
+
+kvp_status kvp_kv_cache_destroy(kvp_kv_cache* c) {
+    return guard([&] { delete c; });
+}
+
+kvp_status kvp_kv_cache_length(const kvp_kv_cache* c, int64_t* length) {
+    return guard([&] {
+        if (!c || !length) throw Error(KVP_ERR_INPUT, "null argument");
+        *length = c->length;
+    });
+}
+
+kvp_status kvp_kv_cache_reset(kvp_kv_cache* c, int64_t length) {
+    return guard([&] {
+        if (!c) throw Error(KVP_ERR_INPUT, "null argument");
+        if (length < 0 || length > c->length) throw Error(KVP_ERR_CACHE, "can only truncate the cache");
+        c->length = length;
+    });
+}
+
+// one rank session over rows [start, start + n) of a cache: the same per-layer schedule as a
+// KVR rank whose prefix [0, start) is already in place
+static void cached_session(kvp_engine* e, kvp_kv_cache* c, const float* rows, int64_t n, int32_t rows_on_device,
+                           bool decode, float* out_rows, float* last_row, float* ms) {
+    auto ok = [](kvp_status st) {
+        if (st != KVP_OK) throw Error(st, kvp_last_error());
+    };
+    if (!c || c->e != e) throw Error(KVP_ERR_INPUT, "cache belongs to another engine");
+    if (n < 1) throw Error(KVP_ERR_INPUT, "no rows");
+    const int64_t start = c->length;
+    if (start + n > c->capacity) throw Error(KVP_ERR_CACHE, "cache capacity exceeded");
+    ok(kvp_rank_begin(e, rows, n, start, c->capacity, rows_on_device, c->ptrs.data()));
+    if (decode) ok(kvp_rank_set_decode(e, 1));
+    for (int64_t l = 0; l < e->s.L; ++l) {
+        ok(kvp_rank_qkv(e, l));
+        ok(kvp_rank_finish(e, l, start + n));
+    }
+    ok(kvp_rank_end(e, out_rows, 0, last_row, ms));
+    c->length = start + n;
+}
+
+kvp_status kvp_prefill_cached(kvp_engine* e, kvp_kv_cache* c, const float* context, int64_t C, float* hidden_out,
+                              float* first_token_hidden, float* ms) {
+    return guard([&] {
+        if (!e || !context) throw Error(KVP_ERR_INPUT, "null argument");
+        cached_session(e, c, context, C, 0, false, hidden_out, first_token_hidden, ms);
+    });
+}
+
+kvp_status kvp_decode(kvp_engine* e, kvp_kv_cache* c, const float* rows, int64_t n_rows, float* out_rows,
+                      float* ms) {
+    return guard([&] {
+        if (!e || !rows) throw Error(KVP_ERR_INPUT, "null argument");
+        if (c && c->length == 0) throw Error(KVP_ERR_CACHE, "decode needs a prefilled cache");
+        if (n_rows > 8) throw Error(KVP_ERR_INPUT, "decode steps take at most 8 new rows");
+        cached_session(e, c, rows, n_rows, 0, true, out_rows, nullptr, ms);
+    });
+}

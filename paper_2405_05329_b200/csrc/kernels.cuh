@@ -107,4 +107,14 @@ void attn_simt_f32(const float* Q, const float* K, const float* V, float* O, con
                    cudaStream_t s);
 void attn_simt_bf16(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShape& sh, cudaStream_t s);
 
+// ---------------------------------------------------------------- decode.cu
+// Decode step (M <= 8 new rows on the prefilled cache): HBM-bound GEMV with gemm_bf16_tc's
+// epilogues, and split-key decode attention (scratch: attn_decode_scratch_floats floats).
+void gemv_bf16(const bf16* X, int64_t M, int64_t K, const bf16* B, int64_t N, const GemmEpilogue& ep,
+               cudaStream_t s);
+int attn_decode_segment(const AttnShape& sh);
+int64_t attn_decode_scratch_floats(const AttnShape& sh);
+void attn_decode_bf16(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShape& sh, float* scratch,
+                      cudaStream_t s);
+
 }  // namespace kvp

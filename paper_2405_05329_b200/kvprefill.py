@@ -124,6 +124,13 @@ _SIGS = {
     "kvp_rank_qkv": (C.c_int, [_P, C.c_int64]),
     "kvp_rank_finish": (C.c_int, [_P, C.c_int64, C.c_int64]),
     "kvp_rank_end": (C.c_int, [_P, _P, C.c_int32, _P, C.POINTER(C.c_float)]),
+    "kvp_rank_set_decode": (C.c_int, [_P, C.c_int32]),
+    "kvp_kv_cache_create": (C.c_int, [_P, C.c_int64, C.POINTER(_P)]),
+    "kvp_kv_cache_destroy": (C.c_int, [_P]),
+    "kvp_kv_cache_length": (C.c_int, [_P, _I64P]),
+    "kvp_kv_cache_reset": (C.c_int, [_P, C.c_int64]),
+    "kvp_prefill_cached": (C.c_int, [_P, _P, _P, C.c_int64, _P, _P, C.POINTER(C.c_float)]),
+    "kvp_decode": (C.c_int, [_P, _P, _P, C.c_int64, _P, C.POINTER(C.c_float)]),
     "kvp_layer_qkv": (C.c_int, [_P, C.c_int64, _P, C.c_int64, _P, _P, _P]),
     "kvp_causal_attention": (C.c_int, [_P, _P, C.c_int64, _P, _P, C.c_int64, C.c_int64, _P]),
     "kvp_layer_finish": (C.c_int, [_P, C.c_int64, _P, C.c_int64, _P, _P, _P, C.c_int64, C.c_int64, _P]),
@@ -478,6 +485,67 @@ def run_device(strategy: Strategy, context_ptr: int, C_: int, partition: Context
                                        len(b) - 1, None, C.c_void_p(hidden_ptr or None),
                                        C.c_void_p(first_token_ptr or None), C.byref(m)), "run_device")
     return ExecutionMetrics._from_c(m)
+
+
+# ------------------------------------------------------------------ KV cache + decode (8f #4)
+class KVCache:
+    """Device K/V cache of `capacity` rows per layer for the prompt + decode steps (new: the
+    reference stops at the first token, engine.hpp:88).  prefill() runs the single-rank prompt
+    phase into it; decode() appends up to 8 rows at the next positions, attending to the whole
+    cache -- the rows a longer serial forward would produce (causal prefix property)."""
+
+    def __init__(self, weights: WeightSet, capacity: int):
+        self.w = weights
+        h = C.c_void_p()
+        _check(lib().kvp_kv_cache_create(weights.handle, int(capacity), C.byref(h)), "kv_cache_create")
+        self._h = h
+        self.capacity = int(capacity)
+
+    @property
+    def length(self) -> int:
+        v = C.c_int64()
+        _check(lib().kvp_kv_cache_length(self._h, C.byref(v)), "kv_cache_length")
+        return int(v.value)
+
+    def reset(self, length: int = 0) -> None:
+        _check(lib().kvp_kv_cache_reset(self._h, int(length)), "kv_cache_reset")
+
+    def prefill(self, context, want_hidden: bool = False):
+        """Prompt phase into the cache (length := C); returns (first_token_hidden [1 x d],
+        hidden_out [C x d] or None, device ms)."""
+        ctx = _f32(context)
+        d = self.w.config.d_model
+        if ctx.ndim != 2 or ctx.shape[1] != d:
+            raise DimensionError("context must be C x d_model")
+        ft = np.empty((1, d), np.float32)
+        hid = np.empty(ctx.shape, np.float32) if want_hidden else None
+        ms = C.c_float()
+        _check(lib().kvp_prefill_cached(self.w.handle, self._h, _vp(ctx), ctx.shape[0], _vp(hid), _vp(ft),
+                                        C.byref(ms)), "prefill_cached")
+        return ft, hid, float(ms.value)
+
+    def decode(self, rows):
+        """Appends rows (n x d, n <= 8) at positions [length, length + n); returns (their final
+        hidden rows, device ms)."""
+        r = _f32(rows)
+        d = self.w.config.d_model
+        if r.ndim != 2 or r.shape[1] != d:
+            raise DimensionError("decode rows must be n x d_model")
+        out = np.empty(r.shape, np.float32)
+        ms = C.c_float()
+        _check(lib().kvp_decode(self.w.handle, self._h, _vp(r), r.shape[0], _vp(out), C.byref(ms)), "decode")
+        return out, float(ms.value)
+
+    def close(self) -> None:
+        if self._h:
+            lib().kvp_kv_cache_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ------------------------------------------------------------------ model.hpp

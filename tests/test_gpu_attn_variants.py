@@ -1,0 +1,67 @@
+"""The tcgen05 attention's alternate code paths (selected by environment variables, read once
+per process) against the oracle and the default path: each variant runs in a subprocess.
+  KVP_ATTN_MMA_WAIT=1     MMA issuer waits for PV(j) before S(j+1) (the default trusts tcgen05
+                          in-order execution; results must be bitwise identical)
+  KVP_ATTN_HD64_TILES=3   head_dim 64 with three query tiles x 96-key tiles
+  KVP_ATTN_POLY=2         part of the exp2 on the FMA pipe (degree-3 polynomial)
+  KVP_PDL=0               no programmatic dependent launch (bitwise identical)"""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import oracle as O
+from paper_2405_05329_b200 import kvprefill as kv
+out = {}
+for d, h in ((1024, 8), (512, 8)):  # head_dim 128 and 64
+    W = kv.init_weights(kv.ModelConfig(d, h, 1 if d == 512 else h, 1, 1, "bf16"))
+    m = O.Model(d, h, 1 if d == 512 else h, 1, 1, "f32", False)
+    C_ = 1000
+    Q = O.random_context(C_, m.q_dim, 31, np.float32) * 4.0
+    K = O.random_context(C_, m.kv_dim, 32, np.float32) * 4.0
+    V = O.random_context(C_, m.kv_dim, 33, np.float32)
+    full = kv.causal_attention(Q, K, V, kv.CausalMask(0, C_), W)
+    part = kv.causal_attention(Q[300:], K, V, kv.CausalMask(300, C_ - 300), W)
+    ref = O.causal_attention(m, Q.astype(np.float64), K.astype(np.float64), V.astype(np.float64), 0)
+    out[str(d)] = {"dev": float(kv.max_rel_dev(full, ref)), "split_equal": bool(np.array_equal(part, full[300:])),
+                   "hash": float(np.float64(full.astype(np.float64).sum()))}
+    W.close()
+print(json.dumps(out))
+"""
+
+
+def _run(env_extra):
+    env = dict(os.environ)
+    env.update(env_extra)
+    r = subprocess.run([sys.executable, "-c", CHILD, ROOT], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+@pytest.fixture(scope="module")
+def default():
+    from paper_2405_05329_b200 import kvprefill as kv
+    if kv.device_count() == 0:
+        pytest.skip("no CUDA device")
+    return _run({})
+
+
+@pytest.mark.parametrize("env,bitwise", [({"KVP_ATTN_MMA_WAIT": "1"}, True), ({"KVP_PDL": "0"}, True),
+                                         ({"KVP_ATTN_HD64_TILES": "3"}, False), ({"KVP_ATTN_POLY": "2"}, False)])
+def test_attention_variant(default, env, bitwise):
+    got = _run(env)
+    for d, res in got.items():
+        assert res["dev"] <= 3e-2, (env, d, res)          # bf16 attention vs the f64 oracle
+        assert res["split_equal"], (env, d)              # split invariance holds in every variant
+        if bitwise or (env.get("KVP_ATTN_HD64_TILES") and d == "1024"):
+            assert res["hash"] == default[d]["hash"], (env, d)
