@@ -5,14 +5,15 @@
 //
 //   gemv_bf16     Y[M x N] = X[M x K] . B[N x K]^T  (B = the K-major weight the tcgen05 GEMM
 //                 uses), f32 accumulation, the SAME epilogues as gemm_bf16_tc (QKV split into the
-//                 cache rows, residual + bf16 copy, ReLU, consumer-side RMSNorm row scale).  One
-//                 warp owns 4 output columns over the whole K (16-byte loads of four weight rows
-//                 in flight per lane, X through the read-only path), so the result is
-//                 deterministic.  Producer-side RMSNorm partials come from a separate tiny kernel
+//                 cache rows, residual + bf16 copy, ReLU, consumer-side RMSNorm row scale).  A
+//                 warp owns 4 output columns over K (or a 1/2, 1/4 slice of K for narrow N, added
+//                 in warp order), 16-byte streaming loads of four weight rows in flight per lane,
+//                 X through the read-only path: deterministic.  Producer-side RMSNorm partials come from a separate tiny kernel
 //                 (M x N floats).
-//   attn_decode   split-key flash decoding: CTA = (kv head, key segment); each warp takes one
-//                 (query head of the group, query row) at a time, lanes split head_dim, online
-//                 softmax over the segment's visible keys; partial (m, l, o) per segment are
+//   attn_decode   split-key flash decoding: one warp per (kv head, key segment), looping over the
+//                 (query head of the group, query row) items; 8 lanes read a key row as 16-byte
+//                 pieces (4 keys per warp step, two steps in flight), each 8-lane group keeps its
+//                 own online softmax, merged by shuffles; partial (m, l, o) per segment are
 //                 merged by a second kernel in segment order (deterministic).
 // Reference semantics: layer_qkv / layer_finish / causal_attention (model.hpp:112-192) for rows
 // at absolute positions [position, position + M).
@@ -39,6 +40,25 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4 v, float (&f)[8]) {
     }
 }
 
+// Launch with programmatic dependent launch (each decode kernel calls griddep_wait() before
+// touching its inputs): the many short kernels of a decode step overlap their launch/prologue
+// with the previous kernel's tail.
+template <typename Kern, typename... Args>
+void pdl_launch(Kern kern, unsigned grid, unsigned block, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    note_launch();
+    cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 struct GvArgs {
     const bf16* X;
     int64_t ldx;
@@ -48,43 +68,52 @@ struct GvArgs {
     float inv_norm_cols;
 };
 
-template <int MM, int KIND>
+template <int MM, int KIND, int KS>
 __global__ void __launch_bounds__(GV_WARPS * 32) gemv_bf16_kernel(GvArgs g) {
+    // KS warps of the CTA split K for the same 4 columns (more bytes in flight for narrow N);
+    // their partials are added in warp order (deterministic)
+    __shared__ float red[GV_WARPS][MM][GV_COLS];
+    ptx::griddep_launch_dependents();
+    ptx::griddep_wait();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n0 = (blockIdx.x * GV_WARPS + warp) * GV_COLS;
-    if (n0 >= g.N) return;
+    const int kg = warp % KS, cg = warp / KS;
+    const int n0 = (blockIdx.x * (GV_WARPS / KS) + cg) * GV_COLS;
+    const int kchunk = ((g.K + KS - 1) / KS + 7) / 8 * 8;
+    const int k_begin = kg * kchunk, k_end = min(g.K, k_begin + kchunk);
     float acc[MM][GV_COLS];
 #pragma unroll
     for (int r = 0; r < MM; ++r)
 #pragma unroll
         for (int c = 0; c < GV_COLS; ++c) acc[r][c] = 0.f;
-    const bf16* wrow[GV_COLS];
+    if (n0 < g.N) {
+        const bf16* wrow[GV_COLS];
 #pragma unroll
-    for (int c = 0; c < GV_COLS; ++c) wrow[c] = g.B + static_cast<int64_t>(min(n0 + c, g.N - 1)) * g.K;
-    // K is a multiple of 8 (host-checked): each lane takes 8 consecutive k per step
-    for (int k = lane * 8; k < g.K; k += 32 * 8 * 2) {
-        uint4 wv[2][GV_COLS];
-        bool has2 = k + 256 < g.K;
+        for (int c = 0; c < GV_COLS; ++c) wrow[c] = g.B + static_cast<int64_t>(min(n0 + c, g.N - 1)) * g.K;
+        // K is a multiple of 8 (host-checked): each lane takes 8 consecutive k per step
+        for (int k = k_begin + lane * 8; k < k_end; k += 32 * 8 * 2) {
+            uint4 wv[2][GV_COLS];
+            const bool has2 = k + 256 < k_end;
 #pragma unroll
-        for (int c = 0; c < GV_COLS; ++c) {
-            wv[0][c] = __ldcs(reinterpret_cast<const uint4*>(wrow[c] + k));  // streamed once
-            if (has2) wv[1][c] = __ldcs(reinterpret_cast<const uint4*>(wrow[c] + k + 256));
-        }
+            for (int c = 0; c < GV_COLS; ++c) {
+                wv[0][c] = __ldcs(reinterpret_cast<const uint4*>(wrow[c] + k));  // streamed once
+                if (has2) wv[1][c] = __ldcs(reinterpret_cast<const uint4*>(wrow[c] + k + 256));
+            }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            if (u == 1 && !has2) break;
-            const int kk = k + u * 256;
+            for (int u = 0; u < 2; ++u) {
+                if (u == 1 && !has2) break;
+                const int kk = k + u * 256;
 #pragma unroll
-            for (int r = 0; r < MM; ++r) {
-                float xf[8];
-                const int rr = r < g.M ? r : g.M - 1;  // padded rows recompute the last one
-                bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(g.X + rr * g.ldx + kk)), xf);
+                for (int r = 0; r < MM; ++r) {
+                    float xf[8];
+                    const int rr = r < g.M ? r : g.M - 1;  // padded rows recompute the last one
+                    bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(g.X + rr * g.ldx + kk)), xf);
 #pragma unroll
-                for (int c = 0; c < GV_COLS; ++c) {
-                    float wf[8];
-                    bf16x8_to_f32(wv[u][c], wf);
+                    for (int c = 0; c < GV_COLS; ++c) {
+                        float wf[8];
+                        bf16x8_to_f32(wv[u][c], wf);
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) acc[r][c] = fmaf(xf[i], wf[i], acc[r][c]);
+                        for (int i = 0; i < 8; ++i) acc[r][c] = fmaf(xf[i], wf[i], acc[r][c]);
+                    }
                 }
             }
         }
@@ -95,7 +124,25 @@ __global__ void __launch_bounds__(GV_WARPS * 32) gemv_bf16_kernel(GvArgs g) {
         for (int c = 0; c < GV_COLS; ++c)
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc[r][c] += __shfl_xor_sync(0xffffffffu, acc[r][c], o);
-    if (lane != 0) return;
+    if constexpr (KS > 1) {
+        if (lane == 0)
+#pragma unroll
+            for (int r = 0; r < MM; ++r)
+#pragma unroll
+                for (int c = 0; c < GV_COLS; ++c) red[warp][r][c] = acc[r][c];
+        __syncthreads();
+        if (kg != 0) return;
+#pragma unroll
+        for (int r = 0; r < MM; ++r)
+#pragma unroll
+            for (int c = 0; c < GV_COLS; ++c) {
+                float v = red[warp][r][c];
+#pragma unroll
+                for (int q = 1; q < KS; ++q) v += red[warp + q][r][c];
+                acc[r][c] = v;
+            }
+    }
+    if (lane != 0 || n0 >= g.N) return;
     const GemmEpilogue& ep = g.ep;
 #pragma unroll
     for (int r = 0; r < MM; ++r) {
@@ -137,6 +184,8 @@ __global__ void __launch_bounds__(GV_WARPS * 32) gemv_bf16_kernel(GvArgs g) {
 // per-row partial sums of squares over 64-column groups of the f32 rows (producer side of the
 // fused RMSNorm): one warp per (row, group)
 __global__ void ssq_parts_kernel(const float* y, int64_t ldy, int M, int N, float* out, int parts) {
+    ptx::griddep_launch_dependents();
+    ptx::griddep_wait();
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= M * parts) return;
     const int r = warp / parts, p = warp % parts;
@@ -149,10 +198,17 @@ __global__ void ssq_parts_kernel(const float* y, int64_t ldy, int M, int N, floa
 
 template <int MM, int KIND>
 void gemv_launch(const GvArgs& g, cudaStream_t s) {
-    const int cols_per_cta = GV_WARPS * GV_COLS;
+    // split K over 1, 2 or 4 warps so that >= ~24 weight-streaming warps land on every SM
+    const int64_t col_warps = (g.N + GV_COLS - 1) / GV_COLS;
+    const int ks = col_warps >= 24 * 148 ? 1 : (col_warps >= 12 * 148 ? 2 : 4);
+    const int cols_per_cta = (GV_WARPS / ks) * GV_COLS;
     const unsigned grid = static_cast<unsigned>((g.N + cols_per_cta - 1) / cols_per_cta);
-    note_launch();
-    gemv_bf16_kernel<MM, KIND><<<grid, GV_WARPS * 32, 0, s>>>(g);
+    if (ks == 1)
+        pdl_launch(gemv_bf16_kernel<MM, KIND, 1>, grid, GV_WARPS * 32, s, g);
+    else if (ks == 2)
+        pdl_launch(gemv_bf16_kernel<MM, KIND, 2>, grid, GV_WARPS * 32, s, g);
+    else
+        pdl_launch(gemv_bf16_kernel<MM, KIND, 4>, grid, GV_WARPS * 32, s, g);
 }
 
 template <int MM>
@@ -166,114 +222,175 @@ void gemv_kind(const GvArgs& g, int kind, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ decode attention
-constexpr int AD_WARPS = 4;
+constexpr int AD_WARPS = 4;  // warps per CTA; every warp owns one key segment
+constexpr int AD_LPK = 8;    // lanes per key: a key row is read as 8 x 16-byte (hd 128) pieces
+constexpr int AD_KPS = 32 / AD_LPK;  // keys per warp step
+
+__device__ __forceinline__ void load_bf16x(const bf16* p, float* f, int n) {
+    // n = 8 or 16 consecutive bf16 (16-byte aligned) -> f32
+    for (int v = 0; v < n / 8; ++v) {
+        float t[8];
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(p + 8 * v), t);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) f[8 * v + e] = t[e];
+    }
+}
 
 template <int HD>
 __global__ void __launch_bounds__(AD_WARPS * 32)
-    attn_decode_kernel(const bf16* Q, const bf16* K, const bf16* V, AttnShape sh, int seg, int n_seg, float sl2,
-                       float* part) {
-    constexpr int PL = HD / 32;  // head_dim elements per lane
+    attn_decode_kernel(const bf16* Q, const bf16* K, const bf16* V, AttnShape sh, int seg, int n_seg, int n_ich,
+                       float sl2, float* part) {
+    constexpr int EPL = HD / AD_LPK;  // head_dim elements per lane (16 or 8)
+    ptx::griddep_launch_dependents();
+    ptx::griddep_wait();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = blockIdx.x / n_seg, sidx = blockIdx.x % n_seg;
+    const int ksub = lane / AD_LPK, sl = lane % AD_LPK;
+    // global warp index -> (kv head, key segment, item chunk): GQA/MQA groups also spread their
+    // (query head, row) items over warps
+    const int wid = blockIdx.x * AD_WARPS + warp;
+    const int ich = wid % n_ich, wseg = wid / n_ich;
+    const int g = wseg / n_seg, sidx = wseg % n_seg;
+    if (g >= sh.n_kv_heads) return;
     const int group = sh.n_heads / sh.n_kv_heads;
     const int64_t k_lo = static_cast<int64_t>(sidx) * seg;
     const int64_t k_hi = k_lo + seg < sh.k_rows ? k_lo + seg : sh.k_rows;
+    const bf16* kb = K + static_cast<int64_t>(g) * HD + sl * EPL;
+    const bf16* vb = V + static_cast<int64_t>(g) * HD + sl * EPL;
     const int items = group * static_cast<int>(sh.q_rows);
-    for (int it = warp; it < items; it += AD_WARPS) {
+    for (int it = ich; it < items; it += n_ich) {
         const int hq = g * group + it % group;  // query head
         const int i = it / group;               // query row
         const int64_t vis = sh.offset + i + 1;  // causal: keys <= offset + i
         const int64_t last = k_hi < vis ? k_hi : vis;
-        float q[PL];
-        {
-            const bf16* qp = Q + i * sh.ldq + static_cast<int64_t>(hq) * HD + lane * PL;
+        float q[EPL];
+        load_bf16x(Q + i * sh.ldq + static_cast<int64_t>(hq) * HD + sl * EPL, q, EPL);
 #pragma unroll
-            for (int e = 0; e < PL; ++e) q[e] = __bfloat162float(qp[e]) * sl2;  // log2-domain scores
-        }
-        float m = -INFINITY, l = 0.f, o[PL];
+        for (int e = 0; e < EPL; ++e) q[e] *= sl2;  // log2-domain scores
+        // every group of AD_LPK lanes keeps its own online-softmax state over its keys
+        float m = -INFINITY, l = 0.f, o[EPL];
 #pragma unroll
-        for (int e = 0; e < PL; ++e) o[e] = 0.f;
-        const bf16* kb = K + static_cast<int64_t>(g) * HD + lane * PL;
-        const bf16* vb = V + static_cast<int64_t>(g) * HD + lane * PL;
-        for (int64_t j = k_lo; j < last; j += 4) {
-            float sc[4], vv[4][PL];
+        for (int e = 0; e < EPL; ++e) o[e] = 0.f;
+        for (int64_t j0 = k_lo; j0 < last; j0 += 2 * AD_KPS) {
+            float kf[2][EPL], vf[2][EPL];
+            bool ok[2];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int64_t jj = j + u < last ? j + u : last - 1;
-                const bf16* kr = kb + jj * sh.ldkv;
-                const bf16* vr = vb + jj * sh.ldkv;
-                float d = 0.f;
+            for (int u = 0; u < 2; ++u) {
+                const int64_t j = j0 + u * AD_KPS + ksub;
+                ok[u] = j < last;
+                const int64_t jj = ok[u] ? j : last - 1;
+                load_bf16x(kb + jj * sh.ldkv, kf[u], EPL);
+                load_bf16x(vb + jj * sh.ldkv, vf[u], EPL);
+            }
 #pragma unroll
-                for (int e = 0; e < PL; ++e) {
-                    d = fmaf(q[e], __bfloat162float(kr[e]), d);
-                    vv[u][e] = __bfloat162float(vr[e]);
+            for (int u = 0; u < 2; ++u) {
+                float sc = 0.f;
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) sc = fmaf(q[e], kf[u][e], sc);
+#pragma unroll
+                for (int off = 1; off < AD_LPK; off <<= 1) sc += __shfl_xor_sync(0xffffffffu, sc, off);
+                if (ok[u]) {
+                    const float mn = fmaxf(m, sc);
+                    const float alpha = exp2f(m - mn), p = exp2f(sc - mn);
+                    l = fmaf(l, alpha, p);
+#pragma unroll
+                    for (int e = 0; e < EPL; ++e) o[e] = fmaf(p, vf[u][e], o[e] * alpha);
+                    m = mn;
                 }
-                sc[u] = d;
             }
+        }
+        // merge the AD_KPS lane groups (lanes sl, sl+8, sl+16, sl+24 hold the same hd slice)
+        float mx = m;
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+        for (int off = AD_LPK; off < 32; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        const float a = (m == -INFINITY) ? 0.f : exp2f(m - mx);
+        l *= a;
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], off);
+        for (int e = 0; e < EPL; ++e) o[e] *= a;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (j + u >= last) break;
-                const float mn = fmaxf(m, sc[u]);
-                const float alpha = exp2f(m - mn), p = exp2f(sc[u] - mn);
-                l = l * alpha + p;
+        for (int off = AD_LPK; off < 32; off <<= 1) {
+            l += __shfl_xor_sync(0xffffffffu, l, off);
 #pragma unroll
-                for (int e = 0; e < PL; ++e) o[e] = fmaf(p, vv[u][e], o[e] * alpha);
-                m = mn;
-            }
+            for (int e = 0; e < EPL; ++e) o[e] += __shfl_xor_sync(0xffffffffu, o[e], off);
         }
         // partial record: [m, l, o[HD]] per (query row, query head, segment)
         float* rec = part + ((static_cast<int64_t>(i) * sh.n_heads + hq) * n_seg + sidx) * (HD + 2);
         if (lane == 0) {
-            rec[0] = m;
+            rec[0] = mx;
             rec[1] = l;
         }
+        if (ksub == 0) {
 #pragma unroll
-        for (int e = 0; e < PL; ++e) rec[2 + lane * PL + e] = o[e];
+            for (int e = 0; e < EPL; ++e) rec[2 + sl * EPL + e] = o[e];
+        }
     }
 }
 
-// merge the segments of each (row, head) in segment order: one warp per (row, head)
+// merge the segments of each (row, head) in segment order: one CTA of HD threads per
+// (row, head); the per-segment weights exp2(m_s - max) go through smem, then thread t sums
+// element t over the segments (independent, coalesced loads)
 template <int HD>
-__global__ void attn_decode_combine(const float* part, int n_seg, int rows, int heads, int64_t ldo, bf16* O) {
-    constexpr int PL = HD / 32;
-    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(HD) attn_decode_combine(const float* part, int n_seg, int rows, int heads,
+                                                          int64_t ldo, bf16* O) {
+    extern __shared__ float wts[];  // [n_seg] weights, then [1] the sum of l
+    ptx::griddep_launch_dependents();
+    ptx::griddep_wait();
+    const int w = blockIdx.x, t = threadIdx.x;
     if (w >= rows * heads) return;
     const int i = w / heads, hq = w % heads;
     const float* base = part + static_cast<int64_t>(w) * n_seg * (HD + 2);
+    __shared__ float red[HD / 32];
     float mx = -INFINITY;
-    for (int s = 0; s < n_seg; ++s) mx = fmaxf(mx, base[s * (HD + 2)]);
-    float l = 0.f, o[PL];
+    for (int s = t; s < n_seg; s += HD) mx = fmaxf(mx, base[s * (HD + 2)]);
 #pragma unroll
-    for (int e = 0; e < PL; ++e) o[e] = 0.f;
-    for (int s = 0; s < n_seg; ++s) {
-        const float* rec = base + s * (HD + 2);
-        if (rec[0] == -INFINITY) continue;  // segment with no visible key
-        const float a = exp2f(rec[0] - mx);
-        l = fmaf(rec[1], a, l);
+    for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    if ((t & 31) == 0) red[t >> 5] = mx;
+    __syncthreads();
+    mx = red[0];
 #pragma unroll
-        for (int e = 0; e < PL; ++e) o[e] = fmaf(rec[2 + lane * PL + e], a, o[e]);
+    for (int q = 1; q < HD / 32; ++q) mx = fmaxf(mx, red[q]);
+    for (int s = t; s < n_seg; s += HD) {
+        const float ms = base[s * (HD + 2)];
+        wts[s] = ms == -INFINITY ? 0.f : exp2f(ms - mx);  // a segment with no visible key weighs 0
     }
-    const float inv = 1.0f / l;
-    bf16* orow = O + i * ldo + static_cast<int64_t>(hq) * HD + lane * PL;
-#pragma unroll
-    for (int e = 0; e < PL; ++e) orow[e] = __float2bfloat16_rn(o[e] * inv);
+    __syncthreads();
+    if (t == 0) {
+        float l = 0.f;
+        for (int s = 0; s < n_seg; ++s) l = fmaf(base[s * (HD + 2) + 1], wts[s], l);
+        wts[n_seg] = l;
+    }
+    float o = 0.f;
+#pragma unroll 8
+    for (int s = 0; s < n_seg; ++s) o = fmaf(base[s * (HD + 2) + 2 + t], wts[s], o);
+    __syncthreads();
+    O[i * ldo + static_cast<int64_t>(hq) * HD + t] = __float2bfloat16_rn(o / wts[n_seg]);
 }
 
 template <int HD>
 void attn_decode_launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShape& sh, float* part,
                         int seg, int n_seg, cudaStream_t s) {
     const float sl2 = (1.0f / sqrtf(static_cast<float>(HD))) * 1.4426950408889634f;
+    // item chunks: enough warps for ~32 per SM when the (kv head, segment) grid is short
+    const int items = (sh.n_heads / sh.n_kv_heads) * static_cast<int>(sh.q_rows);
+    const int base = sh.n_kv_heads * n_seg;
+    int n_ich = (32 * 148 + base - 1) / base;
+    n_ich = n_ich < 1 ? 1 : (n_ich > items ? items : n_ich);
+    const int warps = base * n_ich;
+    pdl_launch(attn_decode_kernel<HD>, static_cast<unsigned>((warps + AD_WARPS - 1) / AD_WARPS), AD_WARPS * 32, s, Q, K,
+               V, sh, seg, n_seg, n_ich, sl2, part);
+    const int cw = static_cast<int>(sh.q_rows) * sh.n_heads;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(cw));
+    cfg.blockDim = dim3(HD);
+    cfg.dynamicSmemBytes = static_cast<size_t>(n_seg + 1) * 4;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
     note_launch();
-    attn_decode_kernel<HD><<<static_cast<unsigned>(sh.n_kv_heads * n_seg), AD_WARPS * 32, 0, s>>>(Q, K, V, sh, seg,
-                                                                                                   n_seg, sl2, part);
-    const int warps = static_cast<int>(sh.q_rows) * sh.n_heads;
-    note_launch();
-    attn_decode_combine<HD><<<static_cast<unsigned>((warps + 3) / 4), 128, 0, s>>>(part, n_seg, static_cast<int>(sh.q_rows),
-                                                                                   sh.n_heads, sh.ldo, O);
+    cudaLaunchKernelEx(&cfg, attn_decode_combine<HD>, static_cast<const float*>(part), n_seg,
+                       static_cast<int>(sh.q_rows), sh.n_heads, sh.ldo, O);
 }
 
 }  // namespace
@@ -294,10 +411,8 @@ void gemv_bf16(const bf16* X, int64_t M, int64_t K, const bf16* B, int64_t N, co
     }
     if (ep.kind == EPI_RESID && ep.ssq_out != nullptr) {
         const int warps = static_cast<int>(M) * ep.ssq_parts;
-        note_launch();
-        ssq_parts_kernel<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, s>>>(ep.outf, ep.ldf, static_cast<int>(M),
-                                                                               static_cast<int>(N), ep.ssq_out,
-                                                                               ep.ssq_parts);
+        pdl_launch(ssq_parts_kernel, static_cast<unsigned>((warps + 7) / 8), 256, s, static_cast<const float*>(ep.outf),
+                   ep.ldf, static_cast<int>(M), static_cast<int>(N), ep.ssq_out, ep.ssq_parts);
     }
 }
 
@@ -308,8 +423,9 @@ int64_t attn_decode_scratch_floats(const AttnShape& sh) {
 }
 
 int attn_decode_segment(const AttnShape& sh) {
-    // enough (kv head, segment) CTAs to keep every SM streaming: ~4 per SM, >= 64 keys each
-    const int64_t want = 4 * 148;
+    // keys per warp: enough (kv head, segment) warps to keep every SM streaming (~32 warps per
+    // SM), at least 64 keys each
+    const int64_t want = 32 * 148;
     int64_t seg = (sh.k_rows * sh.n_kv_heads + want - 1) / want;
     seg = ((seg + 63) / 64) * 64;
     return static_cast<int>(seg < 64 ? 64 : seg);
