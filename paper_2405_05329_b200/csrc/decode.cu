@@ -73,9 +73,28 @@ __global__ void __launch_bounds__(GV_WARPS * 32) gemv_bf16_kernel(GvArgs g) {
     // KS warps of the CTA split K for the same 4 columns (more bytes in flight for narrow N);
     // their partials are added in warp order (deterministic)
     __shared__ float red[GV_WARPS][MM][GV_COLS];
+    __shared__ float row_ss[GV_WARPS][MM];
     ptx::griddep_launch_dependents();
     ptx::griddep_wait();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if constexpr (KIND != EPI_RESID) {
+        if (g.ep.norm_src != nullptr) {  // fused RMSNorm straight from the f32 rows (CTA-wide)
+#pragma unroll
+            for (int r = 0; r < MM; ++r) {
+                const int rr = r < g.M ? r : g.M - 1;
+                const float* src = g.ep.norm_src + rr * g.ep.ld_norm;
+                float ss = 0.f;
+                for (int c = threadIdx.x * 4; c < g.ep.norm_cols; c += GV_WARPS * 32 * 4) {
+                    const float4 v = *reinterpret_cast<const float4*>(src + c);
+                    ss = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, ss))));
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+                if (lane == 0) row_ss[warp][r] = ss;
+            }
+        }
+    }
+    __syncthreads();
     const int kg = warp % KS, cg = warp / KS;
     const int n0 = (blockIdx.x * (GV_WARPS / KS) + cg) * GV_COLS;
     const int kchunk = ((g.K + KS - 1) / KS + 7) / 8 * 8;
@@ -149,7 +168,12 @@ __global__ void __launch_bounds__(GV_WARPS * 32) gemv_bf16_kernel(GvArgs g) {
         if (r >= g.M) break;
         float scale = 1.f;
         if constexpr (KIND != EPI_RESID) {
-            if (ep.ssq_in != nullptr) {
+            if (ep.norm_src != nullptr) {
+                float ss = 0.f;
+#pragma unroll
+                for (int q = 0; q < GV_WARPS; ++q) ss += row_ss[q][r];
+                scale = 1.0f / sqrtf(ss * g.inv_norm_cols + 1e-6f);
+            } else if (ep.ssq_in != nullptr) {
                 float ss = 0.f;
                 for (int q = 0; q < ep.ssq_parts; ++q) ss += ep.ssq_in[r * ep.ssq_parts + q];
                 scale = 1.0f / sqrtf(ss * g.inv_norm_cols + 1e-6f);

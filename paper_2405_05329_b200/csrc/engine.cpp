@@ -473,6 +473,11 @@ static void exec_qkv(const Shape& s, const LayerW& w, RankCtx& R, int64_t c, voi
             ep.ssq_in = R.ssq.as<float>();
             ep.ssq_parts = ssq_parts_for(s.d);
             ep.norm_cols = s.d;
+            if (R.decode) {  // the decode GEMV computes the row scale from the f32 rows
+                ep.ssq_in = nullptr;
+                ep.norm_src = R.h.as<float>();
+                ep.ld_norm = s.d;
+            }
         }
         R.timed(K_GEMM_QKV, gf, 0, [&] {
             if (R.decode)
@@ -532,7 +537,7 @@ static void exec_finish(const Shape& s, const LayerW& w, RankCtx& R, int64_t c, 
         e1.ldr = s.d;
         e1.outb = R.x.as<bf16>();  // bf16(h1): the FFN1 A operand
         e1.ldb = s.d;
-        if (s.rms) {
+        if (s.rms && !R.decode) {
             e1.ssq_out = R.ssq.as<float>();
             e1.ssq_parts = ssq_parts_for(s.d);
         }
@@ -552,6 +557,11 @@ static void exec_finish(const Shape& s, const LayerW& w, RankCtx& R, int64_t c, 
             e2.ssq_in = R.ssq.as<float>();
             e2.ssq_parts = ssq_parts_for(s.d);
             e2.norm_cols = s.d;
+            if (R.decode) {
+                e2.ssq_in = nullptr;
+                e2.norm_src = R.h1.as<float>();
+                e2.ld_norm = s.d;
+            }
         }
         R.timed(K_GEMM_FFN1, 2.0 * c * s.d * s.f, 0, [&] { mm(R.x.as<bf16>(), s.d, w.w1_t, s.f, e2); });
         GemmEpilogue e3;
@@ -562,7 +572,7 @@ static void exec_finish(const Shape& s, const LayerW& w, RankCtx& R, int64_t c, 
         e3.ldr = s.d;
         e3.outb = R.x.as<bf16>();  // bf16(h): the next layer's QKV A operand
         e3.ldb = s.d;
-        if (s.rms) {
+        if (s.rms && !R.decode) {
             e3.ssq_out = R.ssq.as<float>();
             e3.ssq_parts = ssq_parts_for(s.d);
         }

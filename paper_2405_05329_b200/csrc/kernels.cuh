@@ -72,6 +72,10 @@ struct GemmEpilogue {
     const float* ssq_in = nullptr;
     int ssq_parts = 0;
     int64_t norm_cols = 0;
+    // gemv_bf16 only: the consumer computes the row scale from the f32 rows themselves
+    // (norm_src[r, 0:norm_cols], row stride ld_norm) instead of ssq_in partials
+    const float* norm_src = nullptr;
+    int64_t ld_norm = 0;
 };
 inline int ssq_parts_for(int64_t cols) { return static_cast<int>((cols + 63) / 64); }
 void gemm_bf16_tc(const bf16* A, int64_t M, int64_t K, const bf16* B, int64_t N, const GemmEpilogue& ep,
