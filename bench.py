@@ -210,6 +210,34 @@ def run_reference_arm(args, w, rank, world):
 
 
 # ------------------------------------------------------------------ our arm
+def decode_step(W, w, ctx, steps: int = 16) -> dict:
+    """SURVEY 8f #4 (extension): the prompt prefilled into a KVCache, then single-row decode
+    steps on the full cache.  HBM-bound: bytes per step = all projection weights (bf16) + the
+    K/V rows attention reads; device ms per step (median)."""
+    from paper_2405_05329_b200 import kvprefill as kv
+    C = ctx.shape[0]
+    extra = np.random.default_rng(19).uniform(-1.0, 1.0, (steps + 3, w["d_model"])).astype(np.float32)
+    cache = kv.KVCache(W, C + steps + 3)
+    try:
+        cache.prefill(ctx)
+        for i in range(3):
+            cache.decode(extra[i:i + 1])
+        cache.reset(C)
+        times = [cache.decode(extra[i:i + 1])[1] for i in range(steps)]
+    finally:
+        cache.close()
+    d, h, kvh, L = w["d_model"], w["n_heads"], w["n_kv_heads"], w["n_layers"]
+    hd = d // h
+    q, kvd, f = h * hd, kvh * hd, 2 * d
+    nbytes = 2 * L * (d * (q + 2 * kvd) + q * d + 2 * d * f) + 2 * L * 2 * kvd * (C + steps / 2)
+    ms = statistics.median(times)
+    peak = load_peaks()["hbm"]
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    return {"what": f"decode after the {C}-token prompt, 1 row per step (extension, SURVEY 8f #4)",
+            "ms_per_step": ms, "steps": steps, "bytes_per_step": nbytes, "achieved_gbs": gbs,
+            "hbm_peak_gbs": peak, "frac": gbs / peak, "bound": "hbm"}
+
+
 def kv_handoff_bandwidth(b, w, rank, world, local, reps=10):
     """GB/s of the busiest KV-Runahead link (rank p-2 -> p-1 carries K and V rows [0, b_{p-1})
     per layer) measured in isolation with NCCL send/recv, against 900 GB/s per direction of
@@ -361,6 +389,7 @@ def main():
     ap.add_argument("--partition", default="even", choices=["even", "search"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-decode", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     w = dict(WORKLOADS[args.workload])
@@ -481,6 +510,11 @@ def main():
             "clocks": clk.summary(),
             "gpu_launches": launches,
             "e2e": e2e}
+    if n == 1 and not args.no_decode:
+        try:
+            line["decode"] = decode_step(W, w, ctx_host.numpy())
+        except Exception as ex:  # the extension must never break the TTFT line
+            line["decode"] = {"error": str(ex)}
     if n == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(w, C, 1)
