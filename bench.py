@@ -166,7 +166,7 @@ def cpu_baseline(w: dict, C: int, p: int, target_s: float = 12.0):
     import oracle as O
     sample_C = max(p, 32)
     t, kind = time_reference_cpu(w, sample_C, p)
-    while t < target_s / 4 and sample_C < C:  # grow the sample toward ~target_s of CPU work
+    while t < target_s * 0.8 and sample_C < C:  # grow the sample to >= ~10 s of CPU work
         sample_C = min(C, sample_C * 2)
         t, kind = time_reference_cpu(w, sample_C, p)
     full_b = O.even_partition(C, p)

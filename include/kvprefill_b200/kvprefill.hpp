@@ -555,6 +555,46 @@ struct FlatTable {
 };
 }  // namespace detail
 
+// ---------------------------------------------------------------- decode (extension)
+// The reference stops at the first token (engine.hpp:88).  KVCache keeps the prompt's K/V on
+// the device so decode steps can append rows at the next positions.
+template <typename T = float>
+class KVCache {
+  public:
+    KVCache(const WeightSet<T>& w, int64_t capacity) : w_(w) {
+        kvp_kv_cache* c = nullptr;
+        detail::check(kvp_kv_cache_create(w.engine(), capacity, &c), "kv_cache_create");
+        cache_.reset(c, [](kvp_kv_cache* x) { kvp_kv_cache_destroy(x); });
+    }
+    int64_t length() const {
+        int64_t n = 0;
+        detail::check(kvp_kv_cache_length(cache_.get(), &n), "kv_cache_length");
+        return n;
+    }
+    void reset(int64_t length) { detail::check(kvp_kv_cache_reset(cache_.get(), length), "kv_cache_reset"); }
+    // prompt phase into the cache; returns first_token_hidden [1 x d]
+    Matrix<T> prefill(const Matrix<T>& context) {
+        if (context.cols != w_.config.d_model) throw DimensionError("prefill: context width != d_model");
+        Matrix<T> ft(1, w_.config.d_model);
+        detail::check(kvp_prefill_cached(w_.engine(), cache_.get(), context.values.data(), context.rows, nullptr,
+                                         ft.values.data(), nullptr),
+                      "prefill_cached");
+        return ft;
+    }
+    // appends rows (n <= 8) at positions [length, length + n); returns their final hidden rows
+    Matrix<T> decode(const Matrix<T>& rows) {
+        if (rows.cols != w_.config.d_model) throw DimensionError("decode: row width != d_model");
+        Matrix<T> out(rows.rows, rows.cols);
+        detail::check(kvp_decode(w_.engine(), cache_.get(), rows.values.data(), rows.rows, out.values.data(), nullptr),
+                      "decode");
+        return out;
+    }
+
+  private:
+    WeightSet<T> w_;
+    std::shared_ptr<kvp_kv_cache> cache_;
+};
+
 inline std::vector<double> interpolate_partition(const PartitionLookupTable& table, int64_t C) {
     const detail::FlatTable f(table);
     std::vector<double> out(static_cast<size_t>(std::max<int64_t>(table.process_count, 1)));

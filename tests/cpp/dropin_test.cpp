@@ -76,5 +76,17 @@ int main(int argc, char** argv) {
     const auto a = run(Strategy::KVR, big, partition_from_ratios(512, {0.4, 0.3, 0.2, 0.1}), wb);
     const auto b = run(Strategy::Serial, big, even_partition(512, 1), wb);
     expect(a.hidden_out == b.hidden_out, "bf16 tcgen05 path: KVR(p=4) == Serial bitwise");
+    // decode on the prefilled cache (f32 parity mode): rows 9.. equal a longer serial run
+    const auto ctx12 = random_context<float>(12, 8, 21);
+    Matrix<float> head(9, 8), tail(3, 8);
+    std::copy(ctx12.values.begin(), ctx12.values.begin() + 72, head.values.begin());
+    std::copy(ctx12.values.begin() + 72, ctx12.values.end(), tail.values.begin());
+    KVCache<float> cache(w, 12);
+    cache.prefill(head);
+    const auto dec = cache.decode(tail);
+    const auto longer = run(Strategy::Serial, ctx12, even_partition(12, 1), w);
+    expect(std::equal(dec.values.begin(), dec.values.end(), longer.hidden_out.values.begin() + 72) &&
+               cache.length() == 12,
+           "KVCache decode == serial forward over the longer context (f32, bitwise)");
     return failures ? 1 : 0;
 }
