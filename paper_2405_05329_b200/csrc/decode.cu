@@ -18,6 +18,7 @@
 // Reference semantics: layer_qkv / layer_finish / causal_attention (model.hpp:112-192) for rows
 // at absolute positions [position, position + M).
 #include <cmath>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "kernels.cuh"
@@ -68,7 +69,7 @@ struct GvArgs {
     float inv_norm_cols;
 };
 
-template <int MM, int KIND, int KS>
+template <int MM, int KIND, int KS, int U>
 __global__ void __launch_bounds__(GV_WARPS * 32) gemv_bf16_kernel(GvArgs g) {
     // KS warps of the CTA split K for the same 4 columns (more bytes in flight for narrow N);
     // their partials are added in warp order (deterministic)
@@ -109,17 +110,17 @@ __global__ void __launch_bounds__(GV_WARPS * 32) gemv_bf16_kernel(GvArgs g) {
 #pragma unroll
         for (int c = 0; c < GV_COLS; ++c) wrow[c] = g.B + static_cast<int64_t>(min(n0 + c, g.N - 1)) * g.K;
         // K is a multiple of 8 (host-checked): each lane takes 8 consecutive k per step
-        for (int k = k_begin + lane * 8; k < k_end; k += 32 * 8 * 2) {
-            uint4 wv[2][GV_COLS];
-            const bool has2 = k + 256 < k_end;
+        for (int k = k_begin + lane * 8; k < k_end; k += 32 * 8 * U) {
+            // U 16-byte pieces of each of the 4 weight rows in flight per lane
+            uint4 wv[U][GV_COLS];
 #pragma unroll
-            for (int c = 0; c < GV_COLS; ++c) {
-                wv[0][c] = __ldcs(reinterpret_cast<const uint4*>(wrow[c] + k));  // streamed once
-                if (has2) wv[1][c] = __ldcs(reinterpret_cast<const uint4*>(wrow[c] + k + 256));
-            }
+            for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                if (u == 1 && !has2) break;
+                for (int c = 0; c < GV_COLS; ++c)
+                    if (k + u * 256 < k_end) wv[u][c] = __ldcs(reinterpret_cast<const uint4*>(wrow[c] + k + u * 256));
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (k + u * 256 >= k_end) break;
                 const int kk = k + u * 256;
 #pragma unroll
                 for (int r = 0; r < MM; ++r) {
@@ -227,12 +228,25 @@ void gemv_launch(const GvArgs& g, cudaStream_t s) {
     const int ks = col_warps >= 24 * 148 ? 1 : (col_warps >= 12 * 148 ? 2 : 4);
     const int cols_per_cta = (GV_WARPS / ks) * GV_COLS;
     const unsigned grid = static_cast<unsigned>((g.N + cols_per_cta - 1) / cols_per_cta);
-    if (ks == 1)
-        pdl_launch(gemv_bf16_kernel<MM, KIND, 1>, grid, GV_WARPS * 32, s, g);
-    else if (ks == 2)
-        pdl_launch(gemv_bf16_kernel<MM, KIND, 2>, grid, GV_WARPS * 32, s, g);
-    else
-        pdl_launch(gemv_bf16_kernel<MM, KIND, 4>, grid, GV_WARPS * 32, s, g);
+    static const int unroll = [] {
+        const char* e = getenv("KVP_GEMV_UNROLL");
+        return e ? atoi(e) : 2;
+    }();
+    if (unroll == 4) {
+        if (ks == 1)
+            pdl_launch(gemv_bf16_kernel<MM, KIND, 1, 4>, grid, GV_WARPS * 32, s, g);
+        else if (ks == 2)
+            pdl_launch(gemv_bf16_kernel<MM, KIND, 2, 4>, grid, GV_WARPS * 32, s, g);
+        else
+            pdl_launch(gemv_bf16_kernel<MM, KIND, 4, 4>, grid, GV_WARPS * 32, s, g);
+    } else {
+        if (ks == 1)
+            pdl_launch(gemv_bf16_kernel<MM, KIND, 1, 2>, grid, GV_WARPS * 32, s, g);
+        else if (ks == 2)
+            pdl_launch(gemv_bf16_kernel<MM, KIND, 2, 2>, grid, GV_WARPS * 32, s, g);
+        else
+            pdl_launch(gemv_bf16_kernel<MM, KIND, 4, 2>, grid, GV_WARPS * 32, s, g);
+    }
 }
 
 template <int MM>
@@ -246,6 +260,15 @@ void gemv_kind(const GvArgs& g, int kind, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ decode attention
+// target warps per SM for the split-key grid (KVP_DECODE_WPSM tunes it)
+int decode_warps_per_sm() {
+    static const int w = [] {
+        const char* e = getenv("KVP_DECODE_WPSM");
+        return e ? atoi(e) : 32;
+    }();
+    return w > 0 ? w : 32;
+}
+
 constexpr int AD_WARPS = 4;  // warps per CTA; every warp owns one key segment
 constexpr int AD_LPK = 8;    // lanes per key: a key row is read as 8 x 16-byte (hd 128) pieces
 constexpr int AD_KPS = 32 / AD_LPK;  // keys per warp step
@@ -396,7 +419,7 @@ void attn_decode_launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, co
     // item chunks: enough warps for ~32 per SM when the (kv head, segment) grid is short
     const int items = (sh.n_heads / sh.n_kv_heads) * static_cast<int>(sh.q_rows);
     const int base = sh.n_kv_heads * n_seg;
-    int n_ich = (32 * 148 + base - 1) / base;
+    int n_ich = (decode_warps_per_sm() * 148 + base - 1) / base;
     n_ich = n_ich < 1 ? 1 : (n_ich > items ? items : n_ich);
     const int warps = base * n_ich;
     pdl_launch(attn_decode_kernel<HD>, static_cast<unsigned>((warps + AD_WARPS - 1) / AD_WARPS), AD_WARPS * 32, s, Q, K,
@@ -449,7 +472,7 @@ int64_t attn_decode_scratch_floats(const AttnShape& sh) {
 int attn_decode_segment(const AttnShape& sh) {
     // keys per warp: enough (kv head, segment) warps to keep every SM streaming (~32 warps per
     // SM), at least 64 keys each
-    const int64_t want = 32 * 148;
+    const int64_t want = static_cast<int64_t>(decode_warps_per_sm()) * 148;
     int64_t seg = (sh.k_rows * sh.n_kv_heads + want - 1) / want;
     seg = ((seg + 63) / 64) * 64;
     return static_cast<int>(seg < 64 ? 64 : seg);
