@@ -48,6 +48,17 @@ class Transport:
     def _staged(self, t) -> bool:
         return self.backend == "gloo" and t.is_cuda
 
+    def collective_ok(self, executor) -> bool:
+        """All-gather collectives run directly on the executor's tensors: NCCL (device) or gloo
+        with host tensors; gloo with CUDA tensors keeps the staged point-to-point path."""
+        dev = getattr(executor, "device", None)
+        on_cuda = dev is not None and getattr(dev, "type", "cpu") == "cuda"
+        return self.backend == "nccl" or not on_cuda
+
+    def all_gather_rows(self, buf, start: int, stop: int) -> None:
+        """buf[start:stop] of every rank into buf[0:C] (equal chunks, rank order)."""
+        self.dist.all_gather_into_tensor(buf, buf[start:stop].clone(), group=self.group)
+
     def exchange(self, sends, recvs, wait: bool = True):
         """sends: [(tensor, dst)], recvs: [(tensor, src)] -- one batched group.  wait=False
         (sends only) returns the pending works instead of joining them: with NCCL the
@@ -219,6 +230,10 @@ def run_rank(strategy: kv.Strategy, rows, partition: kv.ContextPartition, execut
     out_links = collections.defaultdict(_Link)
     sent_ctr = [0]
     in_flight = []  # KVR handoff sends still on the wire (joined before the rank's result)
+    no_fault = fault is None or fault.kind == kv.FaultInjection.Kind.None_
+    sizes = [b[i + 1] - b[i] for i in range(p)]
+    gather_collective = (strategy == kv.Strategy.TSP and no_fault and p > 1 and len(set(sizes)) == 1
+                         and transport.collective_ok(executor))
     for layer in range(n_layers):
         executor.qkv(layer)
         K, V = executor.kv(layer)
@@ -243,6 +258,20 @@ def run_rank(strategy: kv.Strategy, rows, partition: kv.ContextPartition, execut
                 transport.exchange([], recvs)
                 in_flight.append((transport.exchange(sends, [], wait=False), sends))  # keeps the tensors alive
                 k_rows = stop
+            elif strategy == kv.Strategy.TSP and gather_collective:
+                # no fault can be injected and the chunks are equal: the all-gather is ONE
+                # collective per tensor (NCCL all-gather over NVLink/NVSwitch), in place in the
+                # [C x kv] layer buffer; the accounting is the reference's
+                transport.all_gather_rows(K, start, stop)
+                transport.all_gather_rows(V, start, stop)
+                for peer in range(p):
+                    if peer != rank:
+                        sent_ctr[0] += stop - start
+                        waits += 1
+                        recvd += b[peer + 1] - b[peer]
+                waits += 1
+                barriers += 1
+                k_rows = C_
             elif strategy == kv.Strategy.TSP:
                 sends, recvs = [], []
                 for peer in range(p):
