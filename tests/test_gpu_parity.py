@@ -294,3 +294,48 @@ def test_attention_split_invariance_bitwise(d, h, kvh):
         for lo, hi in ((819, 1433), (1433, 1843), (1843, 2048), (0, 819), (5, 300), (64, 192)):
             part = kv.causal_attention(Q[lo:hi], K[:hi], V[:hi], kv.CausalMask(lo, hi - lo), W)
             assert np.array_equal(part, full[lo:hi]), (scale, lo, hi, np.abs(part - full[lo:hi]).max())
+
+
+# ------------------------------------------------------------ test_model.cpp restatements
+@pytest.mark.parametrize("prec", ["f32", "bf16"])
+@pytest.mark.parametrize("d,h,kvh", [(1024, 8, 8), (512, 8, 1)])
+def test_attention_rows_are_normalised(prec, d, h, kvh):  # test_model.cpp:26-46
+    """softmax rows sum to one: with every V row equal to the same vector the output of every
+    query row IS that vector (masked keys contribute exactly 0)."""
+    W = engine(d, h, kvh, 1, 1, prec)
+    m = oracle_model(d, h, kvh, 1, 1)
+    rows, keys, offset = 150, 400, 250
+    Q = O.random_context(rows, m.q_dim, 3, np.float32) * 3.0
+    K = O.random_context(keys, m.kv_dim, 4, np.float32) * 3.0
+    vrow = O.random_context(1, m.kv_dim, 5, np.float32)
+    V = np.repeat(vrow, keys, axis=0)
+    A = kv.causal_attention(Q, K, V, kv.CausalMask(offset, rows), W)
+    hd = d // h
+    group = h // kvh
+    expect = np.concatenate([vrow[:, (i // group) * hd:(i // group + 1) * hd] for i in range(h)], axis=1)
+    tol = 1e-6 if prec == "f32" else 1e-2  # bf16: V and the output are bf16-rounded
+    assert np.abs(A - expect).max() <= tol * max(1.0, np.abs(expect).max())
+
+
+def test_attention_shape_and_cache_errors():  # test_model.cpp:77-91, 107-127
+    W = engine(1024, 8, 8, 1, 1, "bf16")
+    Q = np.zeros((10, 1024), np.float32)
+    K = np.zeros((20, 1024), np.float32)
+    with pytest.raises(kv.CacheError):  # cache must hold offset + rows keys
+        kv.causal_attention(Q, K, K, kv.CausalMask(15, 10), W)
+    with pytest.raises(kv.DimensionError):
+        kv.causal_attention(Q, K, K[:10], kv.CausalMask(0, 10), W)
+    with pytest.raises(kv.DimensionError):
+        kv.causal_attention(Q, K, K, kv.CausalMask(0, 9), W)
+
+
+@pytest.mark.parametrize("prec", ["f32", "bf16"])
+def test_forward_deterministic_and_rms_variant_differs(prec):  # test_model.cpp:129-153
+    ctx = O.random_context(300, 1024, 8, np.float32)
+    base = engine(1024, 8, 8, 2, 4, prec, False)
+    rms = engine(1024, 8, 8, 2, 4, prec, True)
+    a = kv.run(kv.Strategy.Serial, ctx, kv.even_partition(300, 1), base).hidden_out
+    b = kv.run(kv.Strategy.Serial, ctx, kv.even_partition(300, 1), base).hidden_out
+    c = kv.run(kv.Strategy.Serial, ctx, kv.even_partition(300, 1), rms).hidden_out
+    assert np.array_equal(a, b)
+    assert not np.allclose(a, c)
