@@ -313,7 +313,7 @@ def test_attention_rows_are_normalised(prec, d, h, kvh):  # test_model.cpp:26-46
     hd = d // h
     group = h // kvh
     expect = np.concatenate([vrow[:, (i // group) * hd:(i // group + 1) * hd] for i in range(h)], axis=1)
-    tol = 1e-6 if prec == "f32" else 1e-2  # bf16: V and the output are bf16-rounded
+    tol = 1e-4 if prec == "f32" else 1e-2  # f32: the reference bound; bf16: V and output bf16-rounded
     assert np.abs(A - expect).max() <= tol * max(1.0, np.abs(expect).max())
 
 
