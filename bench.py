@@ -280,8 +280,16 @@ def run_multi(args, w, rank, world, local):
     from paper_2405_05329_b200 import kvprefill as kv
     from paper_2405_05329_b200.distributed import GpuExecutor, Transport, run_rank
 
+    # Test hook (not for measurements): KVP_BENCH_SHARE_GPU=1 puts every rank on cuda:0 and
+    # KVP_BENCH_BACKEND=gloo swaps the transport, so the N>1 code path runs on a 1-GPU box.
+    if os.environ.get("KVP_BENCH_SHARE_GPU") == "1":
+        local = 0
+    backend = os.environ.get("KVP_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
     C = w["C"]
     cfg = kv.ModelConfig(w["d_model"], w["n_heads"], w["n_kv_heads"], w["n_layers"], 1, "bf16", w["rms_norm"])
     W = kv.init_weights(cfg, [local])
