@@ -61,18 +61,22 @@ class Transport:
 
     def exchange(self, sends, recvs, wait: bool = True):
         """sends: [(tensor, dst)], recvs: [(tensor, src)] -- one batched group.  wait=False
-        (sends only) returns the pending works instead of joining them: with NCCL the
-        transfer then runs on the communicator's own stream, overlapping the caller's later
-        kernels; the caller joins the works (and keeps the tensors alive) before reuse."""
+        (sends only) returns (pending works, the tensors actually on the wire) instead of
+        joining them: with NCCL the transfer then runs on the communicator's own stream,
+        overlapping the caller's later kernels; the caller keeps the returned tensors alive
+        (host-staged copies included: gloo does not) until it joins the works."""
         import torch
         dist = self.dist
         staged_recv = []
         ops = []
+        wire = []
         for t, dst in sends:
             if self._staged(t):
                 torch.cuda.current_stream().synchronize()
                 t = t.cpu()
-            ops.append(dist.P2POp(dist.isend, t.contiguous(), dst, self.group))
+            t = t.contiguous()
+            wire.append(t)
+            ops.append(dist.P2POp(dist.isend, t, dst, self.group))
         for t, src in recvs:
             if self._staged(t):
                 host = torch.empty(t.shape, dtype=t.dtype)
@@ -83,7 +87,7 @@ class Transport:
         if not wait:
             if recvs:
                 raise ValueError("deferred exchange is for sends only")
-            return works
+            return works, wire
         for w in works:
             w.wait()
         for host, dev in staged_recv:
@@ -256,7 +260,7 @@ def run_rank(strategy: kv.Strategy, rows, partition: kv.ContextPartition, execut
                 # are never written again, so its transfer to rank i+1 overlaps this rank's
                 # attention/FFN of layer l and the layers after it
                 transport.exchange([], recvs)
-                in_flight.append((transport.exchange(sends, [], wait=False), sends))  # keeps the tensors alive
+                in_flight.append(transport.exchange(sends, [], wait=False))  # (works, tensors kept alive)
                 k_rows = stop
             elif strategy == kv.Strategy.TSP and gather_collective:
                 # no fault can be injected and the chunks are equal: the all-gather is ONE

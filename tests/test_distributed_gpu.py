@@ -73,3 +73,23 @@ def test_two_processes_match_in_process_engine(strategy, boundaries):
     part = kv.ContextPartition(C_, boundaries)
     assert got[0][1]["dot_products"] == [x * 2 for x in kv.dot_product_counts(strat, part)]
     assert sum(got[0][1]["kv_pairs_sent"]) == 2 * kv.traffic_pairs(strat, part)
+
+
+def test_bench_multi_rank_path_on_one_gpu():
+    """bench.py's N>1 path (one process per rank under torchrun: KVR even / KVR-S search / TSP
+    all-gather) end to end on the single GPU of this box, with the test hooks that share cuda:0
+    and use gloo; on a multi-GPU node the same code runs over NCCL."""
+    import json
+    import subprocess
+    env = dict(os.environ, KVP_BENCH_SHARE_GPU="1", KVP_BENCH_BACKEND="gloo")
+    for i, extra in enumerate(([], ["--partition", "search"], ["--strategy", "tsp"])):
+        r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+                            os.path.join(ROOT, "bench.py"), "--gpus", "2", "--workload", "tiny", "--steps", "2",
+                            "--warmup", "3", *extra], capture_output=True, text=True, env=env, timeout=600, cwd=ROOT)
+        assert r.returncode == 0, r.stderr[-3000:]
+        lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+        assert len(lines) == 1, r.stdout[-2000:]
+        d = json.loads(lines[0])
+        assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] > 0
+        assert d["config"]["partition"][0] == 0 and d["config"]["partition"][-1] == 1024
