@@ -33,7 +33,7 @@ def _deps():
 def _compile(src: str, verbose: bool) -> str:
     obj = os.path.join(OUT_DIR, "obj", src + ".o")
     os.makedirs(os.path.dirname(obj), exist_ok=True)
-    cmd = [NVCC, *ARCH, *COMMON, "-c", os.path.join(CSRC, src), "-o", obj]
+    cmd = [NVCC, *ARCH, *COMMON, *os.environ.get("KVP_NVCC_FLAGS", "").split(), "-c", os.path.join(CSRC, src), "-o", obj]
     if src.endswith(".cu"):
         cmd += ["-Xptxas", "-v"] if verbose else []
     else:
