@@ -272,6 +272,7 @@ int decode_warps_per_sm() {
 constexpr int AD_WARPS = 4;  // warps per CTA; every warp owns one key segment
 constexpr int AD_LPK = 8;    // lanes per key: a key row is read as 8 x 16-byte (hd 128) pieces
 constexpr int AD_KPS = 32 / AD_LPK;  // keys per warp step
+constexpr int AD_U = 4;              // warp steps in flight
 
 __device__ __forceinline__ void load_bf16x(const bf16* p, float* f, int n) {
     // n = 8 or 16 consecutive bf16 (16-byte aligned) -> f32
@@ -317,31 +318,51 @@ __global__ void __launch_bounds__(AD_WARPS * 32)
         float m = -INFINITY, l = 0.f, o[EPL];
 #pragma unroll
         for (int e = 0; e < EPL; ++e) o[e] = 0.f;
-        for (int64_t j0 = k_lo; j0 < last; j0 += 2 * AD_KPS) {
-            float kf[2][EPL], vf[2][EPL];
-            bool ok[2];
+        // AD_U key steps (4 keys each) of raw 16-byte K/V pieces in flight per lane, converted
+        // on use; the online softmax rescales o only when the group's running max grows
+        for (int64_t j0 = k_lo; j0 < last; j0 += AD_U * AD_KPS) {
+            uint4 kr[AD_U][EPL / 8], vr[AD_U][EPL / 8];
+            bool ok[AD_U];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < AD_U; ++u) {
                 const int64_t j = j0 + u * AD_KPS + ksub;
                 ok[u] = j < last;
                 const int64_t jj = ok[u] ? j : last - 1;
-                load_bf16x(kb + jj * sh.ldkv, kf[u], EPL);
-                load_bf16x(vb + jj * sh.ldkv, vf[u], EPL);
+#pragma unroll
+                for (int v = 0; v < EPL / 8; ++v) {
+                    kr[u][v] = *reinterpret_cast<const uint4*>(kb + jj * sh.ldkv + 8 * v);
+                    vr[u][v] = *reinterpret_cast<const uint4*>(vb + jj * sh.ldkv + 8 * v);
+                }
             }
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < AD_U; ++u) {
                 float sc = 0.f;
 #pragma unroll
-                for (int e = 0; e < EPL; ++e) sc = fmaf(q[e], kf[u][e], sc);
+                for (int v = 0; v < EPL / 8; ++v) {
+                    float t[8];
+                    bf16x8_to_f32(kr[u][v], t);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) sc = fmaf(q[8 * v + e], t[e], sc);
+                }
 #pragma unroll
                 for (int off = 1; off < AD_LPK; off <<= 1) sc += __shfl_xor_sync(0xffffffffu, sc, off);
                 if (ok[u]) {
-                    const float mn = fmaxf(m, sc);
-                    const float alpha = exp2f(m - mn), p = exp2f(sc - mn);
-                    l = fmaf(l, alpha, p);
+                    if (sc > m) {  // new running max: rescale (exp2(-inf) = 0 on the first key)
+                        const float alpha = exp2f(m - sc);
+                        l *= alpha;
 #pragma unroll
-                    for (int e = 0; e < EPL; ++e) o[e] = fmaf(p, vf[u][e], o[e] * alpha);
-                    m = mn;
+                        for (int e = 0; e < EPL; ++e) o[e] *= alpha;
+                        m = sc;
+                    }
+                    const float p = exp2f(sc - m);
+                    l += p;
+#pragma unroll
+                    for (int v = 0; v < EPL / 8; ++v) {
+                        float t[8];
+                        bf16x8_to_f32(vr[u][v], t);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) o[8 * v + e] = fmaf(p, t[e], o[8 * v + e]);
+                    }
                 }
             }
         }
