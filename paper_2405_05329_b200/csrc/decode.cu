@@ -8,13 +8,15 @@
 //                 cache rows, residual + bf16 copy, ReLU, consumer-side RMSNorm row scale).  A
 //                 warp owns 4 output columns over K (or a 1/2, 1/4 slice of K for narrow N, added
 //                 in warp order), 16-byte streaming loads of four weight rows in flight per lane,
-//                 X through the read-only path: deterministic.  Producer-side RMSNorm partials come from a separate tiny kernel
-//                 (M x N floats).
-//   attn_decode   split-key flash decoding: one warp per (kv head, key segment), looping over the
-//                 (query head of the group, query row) items; 8 lanes read a key row as 16-byte
-//                 pieces (4 keys per warp step, two steps in flight), each 8-lane group keeps its
-//                 own online softmax, merged by shuffles; partial (m, l, o) per segment are
-//                 merged by a second kernel in segment order (deterministic).
+//                 X through the read-only path: deterministic.  In a decode session the
+//                 consumer GEMV computes the RMSNorm row scale from the f32 rows itself
+//                 (norm_src); ssq_parts_kernel serves the partial-sum form otherwise.
+//   attn_decode   split-key flash decoding: one warp per (kv head, key segment, item chunk),
+//                 looping over its (query head of the group, query row) items; 8 lanes read a
+//                 key row as 16-byte pieces (4 keys per warp step, 4 steps in flight), each
+//                 8-lane group keeps its own online softmax (rescaled only when its max grows),
+//                 merged by shuffles; the partial (m, l, o) of the segments are merged by a
+//                 second kernel in segment order (deterministic).
 // Reference semantics: layer_qkv / layer_finish / causal_attention (model.hpp:112-192) for rows
 // at absolute positions [position, position + M).
 #include <cmath>
@@ -275,7 +277,7 @@ constexpr int AD_KPS = 32 / AD_LPK;  // keys per warp step
 constexpr int AD_U = 4;              // warp steps in flight
 
 __device__ __forceinline__ void load_bf16x(const bf16* p, float* f, int n) {
-    // n = 8 or 16 consecutive bf16 (16-byte aligned) -> f32
+    // n = 8 or 16 consecutive bf16 (16-byte aligned) -> f32 (the query row)
     for (int v = 0; v < n / 8; ++v) {
         float t[8];
         bf16x8_to_f32(*reinterpret_cast<const uint4*>(p + 8 * v), t);
