@@ -286,40 +286,47 @@ __device__ __forceinline__ void load_bf16x(const bf16* p, float* f, int n) {
     }
 }
 
-template <int HD>
+template <int HD, int HPW>
 __global__ void __launch_bounds__(AD_WARPS * 32)
     attn_decode_kernel(const bf16* Q, const bf16* K, const bf16* V, AttnShape sh, int seg, int n_seg, int n_ich,
                        float sl2, float* part) {
+    // HPW query heads of one GQA/MQA group per warp item: every K/V piece a lane loads and
+    // converts serves HPW dot products and HPW P.V updates
     constexpr int EPL = HD / AD_LPK;  // head_dim elements per lane (16 or 8)
     ptx::griddep_launch_dependents();
     ptx::griddep_wait();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ksub = lane / AD_LPK, sl = lane % AD_LPK;
-    // global warp index -> (kv head, key segment, item chunk): GQA/MQA groups also spread their
-    // (query head, row) items over warps
+    // global warp index -> (kv head, key segment, item chunk)
     const int wid = blockIdx.x * AD_WARPS + warp;
     const int ich = wid % n_ich, wseg = wid / n_ich;
     const int g = wseg / n_seg, sidx = wseg % n_seg;
     if (g >= sh.n_kv_heads) return;
     const int group = sh.n_heads / sh.n_kv_heads;
+    const int hchunks = (group + HPW - 1) / HPW;
     const int64_t k_lo = static_cast<int64_t>(sidx) * seg;
     const int64_t k_hi = k_lo + seg < sh.k_rows ? k_lo + seg : sh.k_rows;
     const bf16* kb = K + static_cast<int64_t>(g) * HD + sl * EPL;
     const bf16* vb = V + static_cast<int64_t>(g) * HD + sl * EPL;
-    const int items = group * static_cast<int>(sh.q_rows);
+    const int items = hchunks * static_cast<int>(sh.q_rows);
     for (int it = ich; it < items; it += n_ich) {
-        const int hq = g * group + it % group;  // query head
-        const int i = it / group;               // query row
+        const int hc = it % hchunks;  // chunk of HPW query heads of the group
+        const int i = it / hchunks;   // query row
         const int64_t vis = sh.offset + i + 1;  // causal: keys <= offset + i
         const int64_t last = k_hi < vis ? k_hi : vis;
-        float q[EPL];
-        load_bf16x(Q + i * sh.ldq + static_cast<int64_t>(hq) * HD + sl * EPL, q, EPL);
+        float q[HPW][EPL], m[HPW], l[HPW], o[HPW][EPL];
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) q[e] *= sl2;  // log2-domain scores
-        // every group of AD_LPK lanes keeps its own online-softmax state over its keys
-        float m = -INFINITY, l = 0.f, o[EPL];
+        for (int hh = 0; hh < HPW; ++hh) {
+            const int hg = min(hc * HPW + hh, group - 1);  // padded heads recompute the last one
+            load_bf16x(Q + i * sh.ldq + static_cast<int64_t>(g * group + hg) * HD + sl * EPL, q[hh], EPL);
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) o[e] = 0.f;
+            for (int e = 0; e < EPL; ++e) {
+                q[hh][e] *= sl2;  // log2-domain scores
+                o[hh][e] = 0.f;
+            }
+            m[hh] = -INFINITY;  // every group of AD_LPK lanes keeps its own online-softmax state
+            l[hh] = 0.f;
+        }
         // AD_U key steps (4 keys each) of raw 16-byte K/V pieces in flight per lane, converted
         // on use; the online softmax rescales o only when the group's running max grows
         for (int64_t j0 = k_lo; j0 < last; j0 += AD_U * AD_KPS) {
@@ -338,59 +345,77 @@ __global__ void __launch_bounds__(AD_WARPS * 32)
             }
 #pragma unroll
             for (int u = 0; u < AD_U; ++u) {
-                float sc = 0.f;
+                float sc[HPW];
+#pragma unroll
+                for (int hh = 0; hh < HPW; ++hh) sc[hh] = 0.f;
 #pragma unroll
                 for (int v = 0; v < EPL / 8; ++v) {
                     float t[8];
                     bf16x8_to_f32(kr[u][v], t);
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) sc = fmaf(q[8 * v + e], t[e], sc);
+                    for (int hh = 0; hh < HPW; ++hh)
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) sc[hh] = fmaf(q[hh][8 * v + e], t[e], sc[hh]);
                 }
 #pragma unroll
-                for (int off = 1; off < AD_LPK; off <<= 1) sc += __shfl_xor_sync(0xffffffffu, sc, off);
-                if (ok[u]) {
-                    if (sc > m) {  // new running max: rescale (exp2(-inf) = 0 on the first key)
-                        const float alpha = exp2f(m - sc);
-                        l *= alpha;
+                for (int hh = 0; hh < HPW; ++hh)
 #pragma unroll
-                        for (int e = 0; e < EPL; ++e) o[e] *= alpha;
-                        m = sc;
+                    for (int off = 1; off < AD_LPK; off <<= 1) sc[hh] += __shfl_xor_sync(0xffffffffu, sc[hh], off);
+                if (ok[u]) {
+                    float p[HPW];
+#pragma unroll
+                    for (int hh = 0; hh < HPW; ++hh) {
+                        if (sc[hh] > m[hh]) {  // new running max: rescale (exp2(-inf) = 0 first)
+                            const float alpha = exp2f(m[hh] - sc[hh]);
+                            l[hh] *= alpha;
+#pragma unroll
+                            for (int e = 0; e < EPL; ++e) o[hh][e] *= alpha;
+                            m[hh] = sc[hh];
+                        }
+                        p[hh] = exp2f(sc[hh] - m[hh]);
+                        l[hh] += p[hh];
                     }
-                    const float p = exp2f(sc - m);
-                    l += p;
 #pragma unroll
                     for (int v = 0; v < EPL / 8; ++v) {
                         float t[8];
                         bf16x8_to_f32(vr[u][v], t);
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) o[8 * v + e] = fmaf(p, t[e], o[8 * v + e]);
+                        for (int hh = 0; hh < HPW; ++hh)
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) o[hh][8 * v + e] = fmaf(p[hh], t[e], o[hh][8 * v + e]);
                     }
                 }
             }
         }
-        // merge the AD_KPS lane groups (lanes sl, sl+8, sl+16, sl+24 hold the same hd slice)
-        float mx = m;
 #pragma unroll
-        for (int off = AD_LPK; off < 32; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-        const float a = (m == -INFINITY) ? 0.f : exp2f(m - mx);
-        l *= a;
+        for (int hh = 0; hh < HPW; ++hh) {
+            if (hc * HPW + hh >= group) break;
+            const int hq = g * group + hc * HPW + hh;
+            // merge the AD_KPS lane groups (lanes sl, sl+8, sl+16, sl+24 hold the same hd slice)
+            float mx = m[hh];
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) o[e] *= a;
+            for (int off = AD_LPK; off < 32; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+            const float a = (m[hh] == -INFINITY) ? 0.f : exp2f(m[hh] - mx);
+            float lh = l[hh] * a;
+            float oh[EPL];
 #pragma unroll
-        for (int off = AD_LPK; off < 32; off <<= 1) {
-            l += __shfl_xor_sync(0xffffffffu, l, off);
+            for (int e = 0; e < EPL; ++e) oh[e] = o[hh][e] * a;
 #pragma unroll
-            for (int e = 0; e < EPL; ++e) o[e] += __shfl_xor_sync(0xffffffffu, o[e], off);
-        }
-        // partial record: [m, l, o[HD]] per (query row, query head, segment)
-        float* rec = part + ((static_cast<int64_t>(i) * sh.n_heads + hq) * n_seg + sidx) * (HD + 2);
-        if (lane == 0) {
-            rec[0] = mx;
-            rec[1] = l;
-        }
-        if (ksub == 0) {
+            for (int off = AD_LPK; off < 32; off <<= 1) {
+                lh += __shfl_xor_sync(0xffffffffu, lh, off);
 #pragma unroll
-            for (int e = 0; e < EPL; ++e) rec[2 + sl * EPL + e] = o[e];
+                for (int e = 0; e < EPL; ++e) oh[e] += __shfl_xor_sync(0xffffffffu, oh[e], off);
+            }
+            // partial record: [m, l, o[HD]] per (query row, query head, segment)
+            float* rec = part + ((static_cast<int64_t>(i) * sh.n_heads + hq) * n_seg + sidx) * (HD + 2);
+            if (lane == 0) {
+                rec[0] = mx;
+                rec[1] = lh;
+            }
+            if (ksub == 0) {
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) rec[2 + sl * EPL + e] = oh[e];
+            }
         }
     }
 }
@@ -440,13 +465,20 @@ void attn_decode_launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, co
                         int seg, int n_seg, cudaStream_t s) {
     const float sl2 = (1.0f / sqrtf(static_cast<float>(HD))) * 1.4426950408889634f;
     // item chunks: enough warps for ~32 per SM when the (kv head, segment) grid is short
-    const int items = (sh.n_heads / sh.n_kv_heads) * static_cast<int>(sh.q_rows);
+    const int group = sh.n_heads / sh.n_kv_heads;
+    const int hpw = group >= 4 ? (HD == 64 ? 4 : 2) : 1;
+    const int items = ((group + hpw - 1) / hpw) * static_cast<int>(sh.q_rows);
     const int base = sh.n_kv_heads * n_seg;
     int n_ich = (decode_warps_per_sm() * 148 + base - 1) / base;
     n_ich = n_ich < 1 ? 1 : (n_ich > items ? items : n_ich);
     const int warps = base * n_ich;
-    pdl_launch(attn_decode_kernel<HD>, static_cast<unsigned>((warps + AD_WARPS - 1) / AD_WARPS), AD_WARPS * 32, s, Q, K,
-               V, sh, seg, n_seg, n_ich, sl2, part);
+    const unsigned blocks = static_cast<unsigned>((warps + AD_WARPS - 1) / AD_WARPS);
+    if (hpw == 4)
+        pdl_launch(attn_decode_kernel<HD, 4>, blocks, AD_WARPS * 32, s, Q, K, V, sh, seg, n_seg, n_ich, sl2, part);
+    else if (hpw == 2)
+        pdl_launch(attn_decode_kernel<HD, 2>, blocks, AD_WARPS * 32, s, Q, K, V, sh, seg, n_seg, n_ich, sl2, part);
+    else
+        pdl_launch(attn_decode_kernel<HD, 1>, blocks, AD_WARPS * 32, s, Q, K, V, sh, seg, n_seg, n_ich, sl2, part);
     const int cw = static_cast<int>(sh.q_rows) * sh.n_heads;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(cw));
