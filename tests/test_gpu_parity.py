@@ -339,3 +339,19 @@ def test_forward_deterministic_and_rms_variant_differs(prec):  # test_model.cpp:
     c = kv.run(kv.Strategy.Serial, ctx, kv.even_partition(300, 1), rms).hidden_out
     assert np.array_equal(a, b)
     assert not np.allclose(a, c)
+
+
+@pytest.mark.parametrize("prec", ["f32", "bf16"])
+def test_edge_partitions_bitwise(prec):
+    """Ragged edges the reference's partition rules allow: a one-token rank, a one-token prompt,
+    chunks that are not multiples of any tile size -- all bitwise equal to the serial pass."""
+    W = engine(1024, 8, 8, 2, 9, prec, True)
+    for C_, sizes in ((257, [1, 128, 128]), (300, [299, 1]), (129, [64, 1, 64]), (1, [1])):
+        ctx = O.random_context(C_, 1024, 3 + C_, np.float32)
+        serial = kv.run(kv.Strategy.Serial, ctx, kv.even_partition(C_, 1), W)
+        kvr = kv.run(kv.Strategy.KVR, ctx, kv.ContextPartition.from_sizes(sizes), W)
+        assert np.array_equal(serial.hidden_out, kvr.hidden_out), (C_, sizes)
+        assert np.isfinite(serial.hidden_out).all()
+        if len(sizes) > 1 and len(set(sizes)) == 1:
+            tsp = kv.run(kv.Strategy.TSP, ctx, kv.ContextPartition.from_sizes(sizes), W)
+            assert np.array_equal(serial.hidden_out, tsp.hidden_out)
