@@ -100,21 +100,25 @@ class GpuExecutor:
     """One rank's B200 layer executor (kvp_rank_* C-ABI); K/V buffers are torch tensors so
     the transport can address them."""
 
-    def __init__(self, weights: kv.WeightSet, device: int = 0):
+    def __init__(self, weights: kv.WeightSet, device: int = 0, decode_capacity: int = 0):
+        """decode_capacity: extra K/V rows kept free after the prompt for decode steps."""
         import torch
         self.torch = torch
         self.w = weights
         self.cfg = weights.config
         self.device = torch.device("cuda", device)
         self.dtype = torch.bfloat16 if self.cfg.precision == kv.Precision.bf16 else torch.float32
+        self.decode_capacity = int(decode_capacity)
         self._stream = None
 
     def begin(self, rows, start: int, held: int):
         torch = self.torch
         import ctypes as C
         L, kvd = self.cfg.n_layers, self.cfg.kv_dim()
-        self.kvbuf = torch.zeros((L, 2, held, kvd), dtype=self.dtype, device=self.device)
+        self.kvbuf = torch.zeros((L, 2, held + self.decode_capacity, kvd), dtype=self.dtype, device=self.device)
+        self.held = held
         ptrs = (C.c_void_p * (2 * L))(*[self.kvbuf[l, i].data_ptr() for l in range(L) for i in range(2)])
+        self._ptrs = ptrs
         if isinstance(rows, torch.Tensor):
             rows_t = rows.to(self.device, torch.float32).contiguous()
             self._rows = rows_t
@@ -132,6 +136,27 @@ class GpuExecutor:
 
     def stream(self):
         return self.torch.cuda.stream(self._stream)
+
+    def decode(self, rows, position: int):
+        """Decode step on this rank's cache (which holds rows [0, position)): appends the rows
+        (n <= 8) at [position, position + n) with the decode kernels; returns their final
+        hidden rows (host)."""
+        import ctypes as C
+        r = np.ascontiguousarray(rows, dtype=np.float32)
+        n = int(r.shape[0])
+        cap = self.held + self.decode_capacity
+        if position + n > cap:
+            raise kv.CacheError(f"decode needs {position + n} cache rows, the rank holds {cap}")
+        lib = kv.lib()
+        kv._check(lib.kvp_rank_begin(self.w.handle, C.c_void_p(r.ctypes.data), n, position, cap, 0, self._ptrs),
+                  "rank_begin (decode)")
+        kv._check(lib.kvp_rank_set_decode(self.w.handle, 1), "rank_set_decode")
+        for layer in range(self.cfg.n_layers):
+            kv._check(lib.kvp_rank_qkv(self.w.handle, layer), "rank_qkv (decode)")
+            kv._check(lib.kvp_rank_finish(self.w.handle, layer, position + n), "rank_finish (decode)")
+        out = np.empty((n, self.cfg.d_model), np.float32)
+        kv._check(lib.kvp_rank_end(self.w.handle, C.c_void_p(out.ctypes.data), 0, None, None), "rank_end (decode)")
+        return out
 
     def kv(self, layer: int):
         return self.kvbuf[layer, 0], self.kvbuf[layer, 1]
@@ -329,3 +354,13 @@ def run_rank(strategy: kv.Strategy, rows, partition: kv.ContextPartition, execut
     ttft = max(e["ms"] for e in everyone)
     first_token = np.asarray(everyone[-1]["last"], dtype=hidden.dtype)
     return RankResult(hidden, first_token, m, ms, ttft)
+
+
+def decode_on_last_rank(executor, rows, position: int, rank: int, world: int, group=None):
+    """After run_rank(KVR): the last rank holds the whole prompt's KV cache (SURVEY 8e), so it
+    runs the decode step (rows at positions [position, position + n)); the result is broadcast
+    to every rank.  (Extension, SURVEY 8f #4: the reference stops at the first token.)"""
+    import torch.distributed as dist
+    out = [executor.decode(rows, position) if rank == world - 1 else None]
+    dist.broadcast_object_list(out, src=world - 1, group=group)
+    return out[0]

@@ -93,3 +93,48 @@ def test_bench_multi_rank_path_on_one_gpu():
         d = json.loads(lines[0])
         assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] > 0
         assert d["config"]["partition"][0] == 0 and d["config"]["partition"][-1] == 1024
+
+
+def _decode_worker(rank, world, port, outq):
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import oracle as O
+    from paper_2405_05329_b200 import kvprefill as kv
+    from paper_2405_05329_b200.distributed import GpuExecutor, Transport, decode_on_last_rank, run_rank
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    W = kv.init_weights(kv.ModelConfig(1024, 8, 2, 2, 5, "f32", True), [0])
+    b = [0, 200, 331]
+    ctx = O.random_context(335, 1024, 13, np.float32)
+    ex = GpuExecutor(W, 0, decode_capacity=8)
+    run_rank(kv.Strategy.KVR, ctx[b[rank]:b[rank + 1]], kv.ContextPartition(331, b), ex, Transport(), rank, world, 2)
+    out = decode_on_last_rank(ex, ctx[331:335], 331, rank, world)
+    outq.put((rank, out))
+    dist.destroy_process_group()
+
+
+def test_decode_on_last_rank_after_kvr():
+    """The last KVR rank decodes on the prompt's cache (f32 mode: bitwise equal to the serial
+    forward over the longer context), result broadcast to every rank."""
+    sys.path.insert(0, ROOT)
+    import oracle as O
+    from paper_2405_05329_b200 import kvprefill as kv
+    if kv.device_count() == 0:
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_decode_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    W = kv.init_weights(kv.ModelConfig(1024, 8, 2, 2, 5, "f32", True), [0])
+    full = kv.run(kv.Strategy.Serial, O.random_context(335, 1024, 13, np.float32), kv.even_partition(335, 1), W)
+    assert np.array_equal(got[0], got[1])
+    assert np.array_equal(got[1], full.hidden_out[331:335])
