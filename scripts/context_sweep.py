@@ -21,8 +21,12 @@ sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 from paper_2405_05329_b200 import kvprefill as kv  # noqa: E402
 
-Cs = [int(x) for x in sys.argv[1:]] or [1024, 2048, 4096, 8192, 16384, 32768]
-w = dict(bench.WORKLOADS["llama7b-4k"])
+args = sys.argv[1:]
+shape = "llama7b-4k"
+if args and not args[0].isdigit():  # optional shape: llama7b-4k (default) or falcon7b-8k
+    shape = args.pop(0)
+Cs = [int(x) for x in args] or [1024, 2048, 4096, 8192, 16384, 32768]
+w = dict(bench.WORKLOADS[shape])
 d, h, kvh, L = w["d_model"], w["n_heads"], w["n_kv_heads"], w["n_layers"]
 kv_dim = kvh * (d // h)
 peaks = bench.load_peaks()
@@ -44,7 +48,7 @@ for C in Cs:
             times.append(W.last_ttft_ms())
     ms = statistics.median(times)
     F = bench.algorithmic_flops(w, C)
-    line = {"C": C, "p1_ttft_ms": ms, "p1_roofline_ms": F / (peaks["bf16"] * 1e12) * 1e3,
+    line = {"shape": shape.split("-")[0], "C": C, "p1_ttft_ms": ms, "p1_roofline_ms": F / (peaks["bf16"] * 1e12) * 1e3,
             "p1_roofline_frac": F / (peaks["bf16"] * 1e12) / (ms * 1e-3), "algorithmic_tflop": F / 1e12,
             "predicted": {}}
     for p in (2, 4, 8):
