@@ -313,7 +313,9 @@ def run_multi(args, w, rank, world, local):
     rows_host = torch.from_numpy(rows_np).pin_memory()
     rows_dev = rows_host.to(f"cuda:{local}")
     ex = GpuExecutor(W, local)
-    tr = Transport()
+    # peer: the fused handoff (QKV epilogue stores into the receivers' caches over NVLink via
+    # CUDA IPC, stream-ordered flags); msg: NCCL point-to-point / all-gather messages
+    tr = Transport(peer=args.transport == "peer")
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")
 
     def step(rows):
@@ -367,7 +369,10 @@ def run_multi(args, w, rank, world, local):
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded init_weights + uniform context)",
                 "config": {"workload": args.workload, **w, "strategy": args.strategy, "partition": b,
-                           "ranks": world, "transport": "nccl p2p (kvr) / batched p2p all-gather (tsp)",
+                           "ranks": world,
+                           "transport": ("peer memory: QKV-epilogue stores into the receivers' caches over "
+                                         "NVLink (CUDA IPC) + stream-ordered flags" if args.transport == "peer"
+                                         else "nccl p2p (kvr) / all-gather (tsp)"),
                            "l2": "flushed (256 MB write) before every step",
                            "parallelism": f"{args.strategy}-p{world}"},
                 "ttft_roofline_frac": (F / (world * peaks["bf16"] * 1e12)) / (ms * 1e-3),
@@ -397,6 +402,7 @@ def main():
     ap.add_argument("--workload", default="llama7b-4k", choices=sorted(WORKLOADS))
     ap.add_argument("--strategy", default="kvr", choices=["kvr", "tsp"])
     ap.add_argument("--partition", default="even", choices=["even", "search"])
+    ap.add_argument("--transport", default="peer", choices=["peer", "msg"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-decode", action="store_true")

@@ -193,6 +193,33 @@ kvp_status kvp_rank_end(kvp_engine* e, float* out_rows, int32_t out_on_device, f
  * counterpart). */
 kvp_status kvp_rank_set_decode(kvp_engine* e, int32_t on);
 
+/* ------------------------------------------- fused KV handoff over peer memory */
+/* The KV handoff of KVR (rank i -> i+1, engine.hpp:283-288) and the TSP all-gather
+ * (engine.hpp:239-260) fused into the QKV projection: after kvp_rank_set_mirrors, the QKV
+ * GEMM epilogue of every following kvp_rank_qkv stores this rank's K/V rows [start,
+ * start+n_rows) ALSO into n_mirrors other buffers (other ranks' KV caches, mapped with
+ * kvp_ipc_open: NVLink stores, tile by tile, while the projection runs).  mirror_bufs:
+ * n_mirrors * 2*n_layers device pointers (per mirror the same K_0, V_0, K_1, ... layout as
+ * kv_bufs of kvp_rank_begin); n_mirrors <= 8; bf16 only (f32 engines: KVP_ERR_CONFIG).
+ * Cleared by kvp_rank_begin. */
+kvp_status kvp_rank_set_mirrors(kvp_engine* e, int32_t n_mirrors, void* const* mirror_bufs);
+
+/* Cross-process device memory (CUDA IPC): export the allocation holding dev_ptr as a
+ * 64-byte handle plus dev_ptr's byte offset inside it; open a peer's handle in this process
+ * (*dev_ptr = mapped base + offset); close a mapping opened with kvp_ipc_open. */
+kvp_status kvp_ipc_export(const void* dev_ptr, void* handle64, int64_t* offset);
+kvp_status kvp_ipc_open(const void* handle64, int64_t offset, void** dev_ptr);
+kvp_status kvp_ipc_close(void* dev_ptr, int64_t offset);
+
+/* Stream-ordered 32-bit signals (the handoff's "message arrived" in device memory):
+ * kvp_stream_signal writes value to *flag once all earlier work of the stream is done and
+ * visible system-wide (flag may be a peer's memory); kvp_stream_wait holds the stream until
+ * *flag >= value (flag in this device's memory, written by a peer).  kvp_stream_copy is an
+ * async device copy on the stream (peer / IPC pointers allowed). */
+kvp_status kvp_stream_signal(void* stream, void* flag, uint32_t value);
+kvp_status kvp_stream_wait(void* stream, const void* flag, uint32_t value);
+kvp_status kvp_stream_copy(void* stream, void* dst, const void* src, int64_t bytes);
+
 /* ------------------------------------------- KV cache + decode */
 /* The reference stops at the first token (engine.hpp:88); its natural consumer is a decode
  * step on the last rank's full KV cache.  A kvp_kv_cache owns per-layer K/V

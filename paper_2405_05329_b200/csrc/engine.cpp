@@ -338,6 +338,8 @@ struct RankCtx {
     DevBuf h, h1, x, q, a, mid, kv, ssq;
     int64_t held = 0;  // rows per layer K (and V) buffer
     std::vector<void*> ext_kv;  // caller-owned per-layer K/V buffers (multi-process mode)
+    std::vector<void*> mirror_bufs;  // multi-process fused handoff: [n_mirror][L][K,V] peer buffers
+    int n_mirror = 0;
     bool decode = false;        // decode step: HBM-bound GEMV + split-key attention kernels
     DevBuf scratch;             // decode attention partials
     std::vector<cudaEvent_t> ev_send, ev_ready, t_start, t_qkv, t_attn, t_end;
@@ -449,8 +451,18 @@ enum KernelClass { K_NORM = 0, K_GEMM_QKV, K_ATTN, K_GEMM_O, K_GEMM_FFN1, K_GEMM
 static const char* kKernelNames[K_NUM] = {"norm", "gemm_qkv", "attention", "gemm_o", "gemm_ffn1", "gemm_ffn2"};
 
 // layer_qkv (model.hpp:189-192): norm -> fused QKV GEMM; K/V rows land at `kdst`/`vdst`.
+// Where the QKV epilogue also stores this rank's K/V rows (fused KV handoff): pointers at
+// the same rows of other ranks' layer buffers.
+struct KvMirrors {
+    void* k[KVP_MAX_MIRRORS];
+    void* v[KVP_MAX_MIRRORS];
+    int n = 0;
+};
+
 static void exec_qkv(const Shape& s, const LayerW& w, RankCtx& R, int64_t c, void* kdst, void* vdst,
-                     bool prep = true) {
+                     bool prep = true, const KvMirrors* mir = nullptr) {
+    if (mir && mir->n > 0 && (s.prec != KVP_BF16 || R.decode))
+        throw Error(KVP_ERR_CONFIG, "the fused KV handoff needs the bf16 tcgen05 projection");
     const double gf = 2.0 * c * s.d * (s.q + 2 * s.kv);
     if (s.prec == KVP_BF16) {
         // x = bf16(h) and its per-128-column sums of squares; from layer 1 on the previous
@@ -477,6 +489,13 @@ static void exec_qkv(const Shape& s, const LayerW& w, RankCtx& R, int64_t c, voi
                 ep.ssq_in = nullptr;
                 ep.norm_src = R.h.as<float>();
                 ep.ld_norm = s.d;
+            }
+        }
+        if (mir) {
+            ep.n_mirror = mir->n;
+            for (int m = 0; m < mir->n; ++m) {
+                ep.mirror_k[m] = static_cast<bf16*>(mir->k[m]);
+                ep.mirror_v[m] = static_cast<bf16*>(mir->v[m]);
             }
         }
         R.timed(K_GEMM_QKV, gf, 0, [&] {
@@ -622,6 +641,7 @@ struct kvp_engine {
     // multi-process rank session
     bool in_session = false;
     int64_t sess_rows = 0, sess_start = 0, sess_launch0 = 0;
+    bool peer_ok = true;  // every device pair of this engine can address each other's memory
 };
 
 namespace kvp {
@@ -657,6 +677,19 @@ static void run_engine(kvp_engine* e, int32_t strategy, const float* ctx, int64_
         R.marks.clear();
         R.pool_used = 0;
     }
+
+    // Fused KV handoff (bf16): the QKV epilogue stores the rank's K/V rows straight into the
+    // receiving ranks' layer buffers (peer memory over NVLink between GPUs), so the transfer
+    // overlaps the projection tile by tile.  KVR: own rows -> rank r+1 from the epilogue, the
+    // upstream prefix [0, b_r) forwarded by the copy engine as soon as it has landed; TSP:
+    // own rows -> every peer (the all-gather inside the GEMM).  KVP_HANDOFF=copy restores the
+    // copy-engine path (cumulative [0, b_{r+1}) copy after the projection).
+    static const bool handoff_copy = [] {
+        const char* h = getenv("KVP_HANDOFF");
+        return h && std::strcmp(h, "copy") == 0;
+    }();
+    const bool fused = !handoff_copy && s.prec == KVP_BF16 && e->peer_ok && p > 1 &&
+                       (strategy == KVP_KVR || (strategy == KVP_TSP && p - 1 <= KVP_MAX_MIRRORS));
 
     RunMetrics m;
     m.dots.assign(static_cast<size_t>(p), 0);
@@ -752,11 +785,75 @@ static void run_engine(kvp_engine* e, int32_t strategy, const float* ctx, int64_
             uint8_t* K = static_cast<uint8_t*>(R.kv_ptr(s, l, 0));
             uint8_t* V = static_cast<uint8_t*>(R.kv_ptr(s, l, 1));
             KVP_CUDA(cudaEventRecord(R.t_start[l], R.comp));
-            exec_qkv(s, w, R, c, K + start * row_kv, V + start * row_kv, l == 0);
+            KvMirrors mir;
+            if (fused) {
+                for (int64_t peer = 0; peer < p; ++peer) {
+                    if (peer == r || (strategy == KVP_KVR && peer != r + 1)) continue;
+                    RankCtx& P = *e->ranks[static_cast<size_t>(peer)];
+                    mir.k[mir.n] = static_cast<uint8_t*>(P.kv_ptr(s, l, 0)) + start * row_kv;
+                    mir.v[mir.n] = static_cast<uint8_t*>(P.kv_ptr(s, l, 1)) + start * row_kv;
+                    ++mir.n;
+                }
+            }
+            exec_qkv(s, w, R, c, K + start * row_kv, V + start * row_kv, l == 0, &mir);
             KVP_CUDA(cudaGetLastError());
             KVP_CUDA(cudaEventRecord(R.t_qkv[l], R.comp));
             int64_t k_rows;
-            if (strategy == KVP_TSP) {
+            if (strategy == KVP_TSP && fused) {
+                // the all-gather rode the QKV epilogue: t_qkv[l] marks this rank's rows in
+                // every peer's layer buffer
+                for (int64_t peer = 0; peer < p; ++peer) {
+                    if (peer == r) continue;
+                    send(fab.link(r, peer), Msg{GATHER_SHARE, l, r, start, stop, R.t_qkv[l]}, r,
+                         m.sent[static_cast<size_t>(r)]);
+                }
+                std::vector<std::pair<int64_t, int64_t>> segs{{start, stop}};
+                for (int64_t peer = 0; peer < p; ++peer) {
+                    if (peer == r) continue;
+                    Msg in = recv(fab.link(peer, r), GATHER_SHARE, l, m.waits[static_cast<size_t>(r)]);
+                    m.recv[static_cast<size_t>(r)] += in.end - in.start;
+                    KVP_CUDA(cudaStreamWaitEvent(R.comp, in.ready, 0));
+                    segs.emplace_back(in.start, in.end);
+                }
+                std::sort(segs.begin(), segs.end());
+                int64_t next = 0;  // validate_cache_coverage (kv_cache.hpp:41-55)
+                for (auto& sg : segs) {
+                    if (sg.first != next)
+                        throw Error(KVP_ERR_CACHE, "cache gap: expected segment at position " + std::to_string(next));
+                    next = sg.second;
+                }
+                if (next != C) throw Error(KVP_ERR_CACHE, "cache does not cover the context");
+                fab.gate().arrive_and_wait();
+                m.waits[static_cast<size_t>(r)] += 1;
+                k_rows = C;
+            } else if (strategy == KVP_KVR && fused) {
+                Msg in{};
+                if (r > 0) {
+                    in = recv(fab.link(r - 1, r), KV_HANDOFF, l, m.waits[static_cast<size_t>(r)]);
+                    if (in.start != 0 || in.end != start)
+                        throw Error(KVP_ERR_CACHE, "handoff covers [" + std::to_string(in.start) + ", " +
+                                                       std::to_string(in.end) + "), expected prefix [0, " +
+                                                       std::to_string(start) + ")");
+                    m.recv[static_cast<size_t>(r)] += in.end - in.start;
+                    KVP_CUDA(cudaStreamWaitEvent(R.comp, in.ready, 0));
+                }
+                if (r + 1 < p) {
+                    // rows [start, stop) went to rank r+1 from the epilogue; forward the
+                    // upstream prefix [0, start) once it has landed here, on the copy engine
+                    // (independent of this rank's projection), then announce [0, stop)
+                    RankCtx& N = *e->ranks[static_cast<size_t>(r + 1)];
+                    if (r > 0) {
+                        KVP_CUDA(cudaStreamWaitEvent(R.comm, in.ready, 0));
+                        KVP_CUDA(cudaMemcpyAsync(N.kv_ptr(s, l, 0), K, start * row_kv, cudaMemcpyDefault, R.comm));
+                        KVP_CUDA(cudaMemcpyAsync(N.kv_ptr(s, l, 1), V, start * row_kv, cudaMemcpyDefault, R.comm));
+                    }
+                    KVP_CUDA(cudaStreamWaitEvent(R.comm, R.t_qkv[l], 0));
+                    KVP_CUDA(cudaEventRecord(R.ev_send[l], R.comm));
+                    send(fab.link(r, r + 1), Msg{KV_HANDOFF, l, r, 0, stop, R.ev_send[l]}, r,
+                         m.sent[static_cast<size_t>(r)]);
+                }
+                k_rows = stop;
+            } else if (strategy == KVP_TSP) {
                 // all-gather: push own rows [start, stop) into every peer's layer buffer
                 KVP_CUDA(cudaStreamWaitEvent(R.comm, R.t_qkv[l], 0));
                 for (int64_t peer = 0; peer < p; ++peer) {
@@ -959,6 +1056,7 @@ kvp_status kvp_engine_create(const kvp_model_config* cfg, const int32_t* devices
                 if (a != bdev) {
                     int ok = 0;
                     cudaDeviceCanAccessPeer(&ok, a, bdev);
+                    e->peer_ok &= ok != 0;
                     if (ok) {
                         cudaSetDevice(a);
                         cudaDeviceEnablePeerAccess(bdev, 0);
@@ -1270,6 +1368,8 @@ kvp_status kvp_rank_begin(kvp_engine* e, const float* rows, int64_t n_rows, int6
         if (kv_bufs) R.ext_kv.assign(kv_bufs, kv_bufs + 2 * s.L);
         R.profiling = e->profiling;
         R.decode = false;
+        R.n_mirror = 0;
+        R.mirror_bufs.clear();
         R.marks.clear();
         R.pool_used = 0;
         KVP_CUDA(cudaSetDevice(R.device));
@@ -1307,6 +1407,102 @@ kvp_status kvp_rank_set_decode(kvp_engine* e, int32_t on) {
     });
 }
 
+kvp_status kvp_rank_set_mirrors(kvp_engine* e, int32_t n_mirrors, void* const* mirror_bufs) {
+    return guard([&] {
+        std::lock_guard<std::mutex> g(e->mu);
+        RankCtx& R = session_rank(e);
+        if (n_mirrors < 0 || n_mirrors > KVP_MAX_MIRRORS)
+            throw Error(KVP_ERR_INPUT, "at most " + std::to_string(KVP_MAX_MIRRORS) + " mirrors");
+        if (n_mirrors > 0 && e->s.prec != KVP_BF16)
+            throw Error(KVP_ERR_CONFIG, "the fused KV handoff needs the bf16 tcgen05 projection");
+        if (n_mirrors > 0 && !mirror_bufs) throw Error(KVP_ERR_INPUT, "null mirror buffers");
+        R.n_mirror = n_mirrors;
+        R.mirror_bufs.assign(mirror_bufs, mirror_bufs + static_cast<size_t>(n_mirrors) * 2 * e->s.L);
+        for (void* ptr : R.mirror_bufs)
+            if (!ptr) throw Error(KVP_ERR_INPUT, "null mirror buffer");
+    });
+}
+
+}  // extern "C"
+
+namespace kvp {
+// driver-API entry points (no -lcuda at link time: fetched through the runtime)
+template <typename Fn>
+static Fn driver_fn(const char* name) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &ptr, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+        throw Error(KVP_ERR_CUDA, std::string("driver entry point unavailable: ") + name);
+    return reinterpret_cast<Fn>(ptr);
+}
+using StreamValueFn = int (*)(cudaStream_t, unsigned long long, unsigned int, unsigned int);
+using AddrRangeFn = int (*)(unsigned long long*, size_t*, unsigned long long);
+}  // namespace kvp
+
+extern "C" {
+
+kvp_status kvp_ipc_export(const void* dev_ptr, void* handle64, int64_t* offset) {
+    return guard([&] {
+        if (!dev_ptr || !handle64 || !offset) throw Error(KVP_ERR_INPUT, "null argument");
+        static const auto range = driver_fn<AddrRangeFn>("cuMemGetAddressRange");
+        unsigned long long base = 0;
+        size_t size = 0;
+        if (range(&base, &size, reinterpret_cast<unsigned long long>(dev_ptr)) != 0)
+            throw Error(KVP_ERR_CUDA, "not a device allocation");
+        cudaIpcMemHandle_t h;
+        KVP_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+        std::memcpy(handle64, &h, sizeof(h));
+        *offset = static_cast<int64_t>(reinterpret_cast<unsigned long long>(dev_ptr) - base);
+    });
+}
+
+kvp_status kvp_ipc_open(const void* handle64, int64_t offset, void** dev_ptr) {
+    return guard([&] {
+        if (!handle64 || !dev_ptr || offset < 0) throw Error(KVP_ERR_INPUT, "bad argument");
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle64, sizeof(h));
+        void* base = nullptr;
+        KVP_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+        *dev_ptr = static_cast<uint8_t*>(base) + offset;
+    });
+}
+
+kvp_status kvp_ipc_close(void* dev_ptr, int64_t offset) {
+    return guard([&] {
+        if (!dev_ptr) throw Error(KVP_ERR_INPUT, "null pointer");
+        KVP_CUDA(cudaIpcCloseMemHandle(static_cast<uint8_t*>(dev_ptr) - offset));
+    });
+}
+
+kvp_status kvp_stream_signal(void* stream, void* flag, uint32_t value) {
+    return guard([&] {
+        if (!flag) throw Error(KVP_ERR_INPUT, "null flag");
+        static const auto write = driver_fn<StreamValueFn>("cuStreamWriteValue32");
+        // default flags: the write is preceded by a stream-scoped system-wide memory fence
+        if (write(static_cast<cudaStream_t>(stream), reinterpret_cast<unsigned long long>(flag), value, 0) != 0)
+            throw Error(KVP_ERR_CUDA, "cuStreamWriteValue32 failed");
+    });
+}
+
+kvp_status kvp_stream_wait(void* stream, const void* flag, uint32_t value) {
+    return guard([&] {
+        if (!flag) throw Error(KVP_ERR_INPUT, "null flag");
+        static const auto wait = driver_fn<StreamValueFn>("cuStreamWaitValue32");
+        // CU_STREAM_WAIT_VALUE_GEQ (0): values only grow (run epoch * layers + layer + 1)
+        if (wait(static_cast<cudaStream_t>(stream), reinterpret_cast<unsigned long long>(flag), value, 0) != 0)
+            throw Error(KVP_ERR_CUDA, "cuStreamWaitValue32 failed");
+    });
+}
+
+kvp_status kvp_stream_copy(void* stream, void* dst, const void* src, int64_t bytes) {
+    return guard([&] {
+        if (bytes < 0 || ((!dst || !src) && bytes > 0)) throw Error(KVP_ERR_INPUT, "bad copy");
+        if (bytes > 0)
+            KVP_CUDA(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDefault,
+                                     static_cast<cudaStream_t>(stream)));
+    });
+}
+
 kvp_status kvp_rank_kv(kvp_engine* e, int64_t layer, void** K, void** V) {
     return guard([&] {
         std::lock_guard<std::mutex> g(e->mu);
@@ -1327,7 +1523,14 @@ kvp_status kvp_rank_qkv(kvp_engine* e, int64_t layer) {
         uint8_t* K = static_cast<uint8_t*>(R.kv_ptr(s, layer, 0));
         uint8_t* V = static_cast<uint8_t*>(R.kv_ptr(s, layer, 1));
         KVP_CUDA(cudaEventRecord(R.t_start[layer], R.comp));
-        exec_qkv(s, w, R, e->sess_rows, K + e->sess_start * row_kv, V + e->sess_start * row_kv, layer == 0);
+        KvMirrors mir;
+        for (int m = 0; m < R.n_mirror; ++m) {
+            const size_t at = (static_cast<size_t>(m) * s.L + static_cast<size_t>(layer)) * 2;
+            mir.k[m] = static_cast<uint8_t*>(R.mirror_bufs[at]) + e->sess_start * row_kv;
+            mir.v[m] = static_cast<uint8_t*>(R.mirror_bufs[at + 1]) + e->sess_start * row_kv;
+        }
+        mir.n = R.decode ? 0 : R.n_mirror;
+        exec_qkv(s, w, R, e->sess_rows, K + e->sess_start * row_kv, V + e->sess_start * row_kv, layer == 0, &mir);
         KVP_CUDA(cudaGetLastError());
         KVP_CUDA(cudaEventRecord(R.t_qkv[layer], R.comp));
     });

@@ -108,6 +108,9 @@ struct EpiArgs {
     const float* ssq_in;
     int ssq_parts;
     float inv_norm_cols;
+    bf16* mk[8];  // EPI_QKV mirrors of the K / V columns (GemmEpilogue::mirror_k/v)
+    bf16* mv[8];
+    int n_mirror;
 };
 
 // QKV split / ReLU / plain bf16 store of one 32-column chunk (lane = row).
@@ -117,6 +120,8 @@ __device__ __forceinline__ void store_chunk(const EpiArgs& ep, int64_t row, int6
     const bool full = col0 + 32 <= N;
     {
         bf16* o;
+        int region = 0;  // EPI_QKV: 1 = K, 2 = V chunk (also stored to the mirrors)
+        int64_t region_off = 0;
         if constexpr (KIND == EPI_QKV) {
             // chunks straddling the Q|K|V column boundaries (q or kv not a multiple of 32)
             // take the per-element path
@@ -128,7 +133,12 @@ __device__ __forceinline__ void store_chunk(const EpiArgs& ep, int64_t row, int6
                     const int64_t c = col0 + j;
                     bf16* dst = c < e0 ? ep.out0 + row * ep.ld0 + c
                                        : (c < e1 ? ep.out1 + row * ep.ld1 + (c - e0) : ep.out2 + row * ep.ld2 + (c - e1));
-                    *dst = __float2bfloat16_rn(__uint_as_float(r[j]) * row_scale);
+                    const bf16 val = __float2bfloat16_rn(__uint_as_float(r[j]) * row_scale);
+                    *dst = val;
+#pragma unroll
+                    for (int m = 0; m < 8; ++m)
+                        if (m < ep.n_mirror && c >= e0)
+                            *(c < e1 ? ep.mk[m] + row * ep.ld1 + (c - e0) : ep.mv[m] + row * ep.ld2 + (c - e1)) = val;
                 }
                 return;
             }
@@ -136,8 +146,12 @@ __device__ __forceinline__ void store_chunk(const EpiArgs& ep, int64_t row, int6
                 o = ep.out0 + row * ep.ld0 + col0;
             } else if (col0 < ep.n0 + ep.n1) {
                 o = ep.out1 + row * ep.ld1 + (col0 - ep.n0);
+                region_off = row * ep.ld1 + (col0 - ep.n0);
+                region = 1;
             } else {
                 o = ep.out2 + row * ep.ld2 + (col0 - ep.n0 - ep.n1);
+                region_off = row * ep.ld2 + (col0 - ep.n0 - ep.n1);
+                region = 2;
             }
         } else {
             o = ep.out0 + row * ep.ld0 + col0;
@@ -157,11 +171,22 @@ __device__ __forceinline__ void store_chunk(const EpiArgs& ep, int64_t row, int6
                 pk.z = ptx::pack_bf16(v[j + 4], v[j + 5]);
                 pk.w = ptx::pack_bf16(v[j + 6], v[j + 7]);
                 *reinterpret_cast<uint4*>(o + j) = pk;
+                if constexpr (KIND == EPI_QKV)
+#pragma unroll
+                    for (int m = 0; m < 8; ++m)
+                        if (region && m < ep.n_mirror)
+                            *reinterpret_cast<uint4*>((region == 1 ? ep.mk[m] : ep.mv[m]) + region_off + j) = pk;
             }
         } else {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-                if (col0 + j < N) o[j] = __float2bfloat16_rn(v[j]);
+                if (col0 + j < N) {
+                    o[j] = __float2bfloat16_rn(v[j]);
+                    if constexpr (KIND == EPI_QKV)
+#pragma unroll
+                        for (int m = 0; m < 8; ++m)
+                            if (region && m < ep.n_mirror) (region == 1 ? ep.mk[m] : ep.mv[m])[region_off + j] = o[j];
+                }
         }
     }
 }
@@ -576,7 +601,12 @@ template <int BN, int NCTA>
 void dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tbh, int M, int N, int K,
               const GemmEpilogue& g, cudaStream_t s) {
     EpiArgs ep{g.out0, g.ld0, g.n0, g.out1, g.ld1, g.n1, g.out2, g.ld2, g.outf, g.ldf, g.resid, g.ldr,
-               g.outb, g.ldb, g.ssq_out, g.ssq_in, g.ssq_parts, g.norm_cols ? 1.0f / static_cast<float>(g.norm_cols) : 0.f};
+               g.outb, g.ldb, g.ssq_out, g.ssq_in, g.ssq_parts, g.norm_cols ? 1.0f / static_cast<float>(g.norm_cols) : 0.f,
+               {}, {}, g.kind == EPI_QKV ? g.n_mirror : 0};
+    for (int m = 0; m < ep.n_mirror; ++m) {
+        ep.mk[m] = g.mirror_k[m];
+        ep.mv[m] = g.mirror_v[m];
+    }
     switch (g.kind) {
         case EPI_QKV: launch_tc<BN, EPI_QKV, NCTA>(ta, tb, tbh, M, N, K, ep, s); break;
         case EPI_RESID: launch_tc<BN, EPI_RESID, NCTA>(ta, tb, tbh, M, N, K, ep, s); break;

@@ -76,7 +76,15 @@ struct GemmEpilogue {
     // (norm_src[r, 0:norm_cols], row stride ld_norm) instead of ssq_in partials
     const float* norm_src = nullptr;
     int64_t ld_norm = 0;
+    // EPI_QKV (tcgen05 GEMM) only: the K and V columns are ALSO stored into up to
+    // KVP_MAX_MIRRORS other buffers with out1/out2's row stride -- other ranks' KV caches
+    // (peer memory over NVLink, or IPC-mapped), so the KV handoff rides the projection's
+    // epilogue tile by tile instead of a copy after it
+    bf16* mirror_k[8] = {};
+    bf16* mirror_v[8] = {};
+    int n_mirror = 0;
 };
+constexpr int KVP_MAX_MIRRORS = 8;
 inline int ssq_parts_for(int64_t cols) { return static_cast<int>((cols + 63) / 64); }
 void gemm_bf16_tc(const bf16* A, int64_t M, int64_t K, const bf16* B, int64_t N, const GemmEpilogue& ep,
                   cudaStream_t s);

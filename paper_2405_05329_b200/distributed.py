@@ -39,11 +39,26 @@ class Transport:
     tensors stay on the GPU and the ops are ordered on the caller's current CUDA stream.  With
     gloo, CUDA tensors are staged through host memory (shared-GPU / CPU test runs)."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, peer: Optional[bool] = None):
+        """peer: move K/V through peer memory (CUDA IPC mappings of the other ranks' caches,
+        NVLink between GPUs) instead of messages -- the QKV epilogue stores the rows straight
+        into the receiver's cache and stream-ordered flags say they have landed; the group
+        then only carries host metadata.  Default: KVP_TRANSPORT=peer (explicit opt-out:
+        KVP_TRANSPORT=msg)."""
+        import os
         import torch.distributed as dist
         self.dist = dist
         self.group = group
         self.backend = dist.get_backend(group)
+        if peer is None:
+            peer = os.environ.get("KVP_TRANSPORT", "") == "peer"
+        self.peer = bool(peer)
+
+    def peer_ok(self, executor) -> bool:
+        """The fused peer-memory handoff needs bf16 CUDA executors (tcgen05 QKV epilogue)."""
+        dev = getattr(executor, "device", None)
+        return (self.peer and dev is not None and getattr(dev, "type", "cpu") == "cuda"
+                and executor.cfg.precision == kv.Precision.bf16)
 
     def _staged(self, t) -> bool:
         return self.backend == "gloo" and t.is_cuda
@@ -110,12 +125,17 @@ class GpuExecutor:
         self.dtype = torch.bfloat16 if self.cfg.precision == kv.Precision.bf16 else torch.float32
         self.decode_capacity = int(decode_capacity)
         self._stream = None
+        self.kvbuf = None
+        self.peer = None  # _PeerSession of the fused peer-memory handoff
 
     def begin(self, rows, start: int, held: int):
         torch = self.torch
         import ctypes as C
         L, kvd = self.cfg.n_layers, self.cfg.kv_dim()
-        self.kvbuf = torch.zeros((L, 2, held + self.decode_capacity, kvd), dtype=self.dtype, device=self.device)
+        shape = (L, 2, held + self.decode_capacity, kvd)
+        if self.kvbuf is None or tuple(self.kvbuf.shape) != shape:
+            # kept across runs of the same shape: peers hold IPC mappings of it
+            self.kvbuf = torch.zeros(shape, dtype=self.dtype, device=self.device)
         self.held = held
         ptrs = (C.c_void_p * (2 * L))(*[self.kvbuf[l, i].data_ptr() for l in range(L) for i in range(2)])
         self._ptrs = ptrs
@@ -174,11 +194,110 @@ class GpuExecutor:
         kv._check(kv.lib().kvp_rank_end(self.w.handle, C.c_void_p(out.ctypes.data), 0, None, C.byref(ms)), "rank_end")
         return out, float(ms.value)
 
+    def raw_stream(self) -> int:
+        return self._stream.cuda_stream
+
+    def set_mirrors(self, bufs):
+        """bufs: per mirror, 2L device pointers (K_0, V_0, ...) of another rank's cache."""
+        import ctypes as C
+        flat = [ptr for mirror in bufs for ptr in mirror]
+        arr = (C.c_void_p * max(1, len(flat)))(*flat)
+        kv._check(kv.lib().kvp_rank_set_mirrors(self.w.handle, len(bufs), arr), "rank_set_mirrors")
+
     def header(self, values):
         return self.torch.tensor(values, dtype=self.torch.int64, device=self.device)
 
     def empty_header(self):
         return self.torch.zeros(HDR_LEN, dtype=self.torch.int64, device=self.device)
+
+
+# ------------------------------------------------------------------ peer-memory handoff
+_FLAG_SLOTS = 64  # one int32 per source rank (TSP) / {own rows, forwarded prefix} (KVR)
+
+
+def _ipc_export(ptr: int):
+    import ctypes as C
+    h = (C.c_ubyte * 64)()
+    off = C.c_int64()
+    kv._check(kv.lib().kvp_ipc_export(C.c_void_p(ptr), h, C.byref(off)), "ipc_export")
+    return bytes(h), int(off.value)
+
+
+class _PeerSession:
+    """CUDA IPC mappings of the other ranks' KV caches and flag words (opened once per
+    partition / strategy, re-used by every run) plus a monotonically growing run epoch: the
+    flag value of layer l in run e is e*L + l + 1, so a GEQ wait never needs a reset."""
+
+    def __init__(self, executor):
+        torch = executor.torch
+        self.ex = executor
+        self.flags = torch.zeros(_FLAG_SLOTS, dtype=torch.int32, device=executor.device)
+        self.comm = torch.cuda.Stream(device=executor.device)
+        self.epoch = 0
+        self.key = None
+        self.bases = {}     # handle bytes -> mapped base pointer
+        self.peers = {}     # rank -> {"kv": [2L ptrs], "flags": ptr}
+
+    def _open(self, handle: bytes) -> int:
+        import ctypes as C
+        if handle not in self.bases:
+            ptr = C.c_void_p()
+            kv._check(kv.lib().kvp_ipc_open(handle, 0, C.byref(ptr)), "ipc_open")
+            self.bases[handle] = int(ptr.value)
+        return self.bases[handle]
+
+    def close(self):
+        import ctypes as C
+        for base in self.bases.values():
+            kv.lib().kvp_ipc_close(C.c_void_p(base), 0)
+        self.bases.clear()
+        self.peers.clear()
+
+    def setup(self, key, rank: int, world: int, group):
+        """Exchange handles when the partition / strategy (hence every rank's buffers)
+        changed -- the same decision on every rank, so the collective is always matched."""
+        import torch.distributed as dist
+        if key == self.key:
+            return
+        ex = self.ex
+        torch = ex.torch
+        torch.cuda.current_stream(ex.device).synchronize()
+        mine = {"kv": _ipc_export(ex.kvbuf.data_ptr()), "rows": int(ex.kvbuf.shape[2]),
+                "flags": _ipc_export(self.flags.data_ptr()), "pid": __import__("os").getpid()}
+        everyone = [None] * world
+        dist.all_gather_object(everyone, mine, group=group)
+        self.close()
+        L, kvd = ex.cfg.n_layers, ex.cfg.kv_dim()
+        es = ex.kvbuf.element_size()
+        for j, info in enumerate(everyone):
+            if j == rank:
+                continue
+            base = self._open(info["kv"][0]) + info["kv"][1]
+            plane = info["rows"] * kvd * es
+            self.peers[j] = {"kv": [base + (2 * l + i) * plane for l in range(L) for i in range(2)],
+                             "flags": self._open(info["flags"][0]) + info["flags"][1]}
+        self.key = key
+
+    def flag(self, j: int, slot: int) -> int:
+        return self.peers[j]["flags"] + 4 * slot
+
+    def my_flag(self, slot: int) -> int:
+        return self.flags.data_ptr() + 4 * slot
+
+
+def _signal(stream: int, flag: int, value: int):
+    import ctypes as C
+    kv._check(kv.lib().kvp_stream_signal(C.c_void_p(stream), C.c_void_p(flag), value), "stream_signal")
+
+
+def _wait(stream: int, flag: int, value: int):
+    import ctypes as C
+    kv._check(kv.lib().kvp_stream_wait(C.c_void_p(stream), C.c_void_p(flag), value), "stream_wait")
+
+
+def _copy(stream: int, dst: int, src: int, nbytes: int):
+    import ctypes as C
+    kv._check(kv.lib().kvp_stream_copy(C.c_void_p(stream), C.c_void_p(dst), C.c_void_p(src), nbytes), "stream_copy")
 
 
 # ------------------------------------------------------------------ the rank driver
@@ -263,9 +382,62 @@ def run_rank(strategy: kv.Strategy, rows, partition: kv.ContextPartition, execut
     sizes = [b[i + 1] - b[i] for i in range(p)]
     gather_collective = (strategy == kv.Strategy.TSP and no_fault and p > 1 and len(set(sizes)) == 1
                          and transport.collective_ok(executor))
+    # fused peer-memory handoff (no fault injected: faults are message edits, so they keep
+    # the message path): the QKV epilogue stores this rank's K/V rows into the receivers'
+    # caches; KVR forwards the upstream prefix with one copy-engine copy per tensor as soon
+    # as it has landed; stream-ordered flags replace the messages
+    use_peer = (no_fault and p > 1 and strategy in (kv.Strategy.KVR, kv.Strategy.TSP) and transport.peer_ok(executor)
+            and (strategy == kv.Strategy.KVR or p - 1 <= 8))
+    if use_peer:
+        if executor.peer is None:
+            executor.peer = _PeerSession(executor)
+        ps = executor.peer
+        ps.setup((tuple(b), int(strategy), world), rank, world, group)
+        ps.epoch += 1
+        L = n_layers
+        es = executor.kvbuf.element_size()
+        row_bytes = executor.cfg.kv_dim() * es
+        comp, comm = executor.raw_stream(), ps.comm.cuda_stream
+        targets = ([rank + 1] if rank + 1 < p else []) if strategy == kv.Strategy.KVR else \
+            [j for j in range(p) if j != rank]
+        executor.set_mirrors([ps.peers[j]["kv"] for j in targets])
     for layer in range(n_layers):
         executor.qkv(layer)
         K, V = executor.kv(layer)
+        if use_peer:
+            v = ps.epoch * L + layer + 1
+            if strategy == kv.Strategy.KVR:
+                OWN, PREFIX = 0, 1
+                if rank + 1 < p:
+                    _signal(comp, ps.flag(rank + 1, OWN), v)  # rows [start, stop) are at rank+1
+                    sent_ctr[0] += stop
+                if rank > 0:
+                    waits += 1
+                    recvd += start
+                    for st in ((comp, comm) if rank + 1 < p else (comp,)):
+                        _wait(st, ps.my_flag(OWN), v)
+                        if rank > 1:
+                            _wait(st, ps.my_flag(PREFIX), v)
+                    if rank + 1 < p:  # forward [0, start) on the copy engine
+                        dst = ps.peers[rank + 1]["kv"]
+                        _copy(comm, dst[2 * layer], K.data_ptr(), start * row_bytes)
+                        _copy(comm, dst[2 * layer + 1], V.data_ptr(), start * row_bytes)
+                        _signal(comm, ps.flag(rank + 1, PREFIX), v)
+                k_rows = stop
+            else:
+                for j in targets:
+                    _signal(comp, ps.flag(j, rank), v)
+                for j in targets:
+                    _wait(comp, ps.my_flag(j), v)
+                    sent_ctr[0] += stop - start
+                    waits += 1
+                    recvd += b[j + 1] - b[j]
+                waits += 1
+                barriers += 1
+                k_rows = C_
+            dots += c * k_rows
+            executor.finish(layer, k_rows)
+            continue
         with executor.stream():
             if strategy == kv.Strategy.KVR:
                 sends, recvs = [], []
@@ -328,6 +500,8 @@ def run_rank(strategy: kv.Strategy, rows, partition: kv.ContextPartition, execut
         for works, _ in in_flight:
             for w in works:
                 w.wait()
+        if use_peer:  # the prefix forwards are part of this rank's run
+            executor._stream.wait_stream(ps.comm)
     hidden, ms = executor.end()
     sent = sent_ctr[0]
 

@@ -125,6 +125,13 @@ _SIGS = {
     "kvp_rank_finish": (C.c_int, [_P, C.c_int64, C.c_int64]),
     "kvp_rank_end": (C.c_int, [_P, _P, C.c_int32, _P, C.POINTER(C.c_float)]),
     "kvp_rank_set_decode": (C.c_int, [_P, C.c_int32]),
+    "kvp_rank_set_mirrors": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_void_p)]),
+    "kvp_ipc_export": (C.c_int, [_P, _P, C.POINTER(C.c_int64)]),
+    "kvp_ipc_open": (C.c_int, [_P, C.c_int64, C.POINTER(C.c_void_p)]),
+    "kvp_ipc_close": (C.c_int, [_P, C.c_int64]),
+    "kvp_stream_signal": (C.c_int, [_P, _P, C.c_uint32]),
+    "kvp_stream_wait": (C.c_int, [_P, _P, C.c_uint32]),
+    "kvp_stream_copy": (C.c_int, [_P, _P, _P, C.c_int64]),
     "kvp_kv_cache_create": (C.c_int, [_P, C.c_int64, C.POINTER(_P)]),
     "kvp_kv_cache_destroy": (C.c_int, [_P]),
     "kvp_kv_cache_length": (C.c_int, [_P, _I64P]),

@@ -23,7 +23,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, strategy, boundaries, outq):
+def _worker(rank, world, port, strategy, runs, peer, outq):
     sys.path.insert(0, ROOT)
     import torch
     import torch.distributed as dist
@@ -35,44 +35,77 @@ def _worker(rank, world, port, strategy, boundaries, outq):
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     W = kv.init_weights(kv.ModelConfig(1024, 8, 2, 2, 5, "bf16", True), [0])
-    C_ = boundaries[-1]
-    ctx = O.random_context(C_, 1024, 11, np.float32)
+    ex = GpuExecutor(W, 0)
+    tr = Transport(peer=peer)
     strat = kv.Strategy.KVR if strategy == "kvr" else kv.Strategy.TSP
-    res = run_rank(strat, ctx[boundaries[rank]:boundaries[rank + 1]], kv.ContextPartition(C_, boundaries),
-                   GpuExecutor(W, 0), Transport(), rank, world, 2)
-    outq.put((rank, res.hidden_rows, res.metrics.__dict__))
+    out = []
+    for boundaries in runs:  # consecutive runs on one executor (buffer / mapping reuse)
+        C_ = boundaries[-1]
+        ctx = O.random_context(C_, 1024, 11, np.float32)
+        res = run_rank(strat, ctx[boundaries[rank]:boundaries[rank + 1]], kv.ContextPartition(C_, boundaries),
+                       ex, tr, rank, world, 2)
+        out.append((res.hidden_rows, res.metrics.__dict__))
+    outq.put((rank, out))
     dist.destroy_process_group()
+
+
+def _run_procs(world, strategy, runs, peer):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, strategy, runs, peer, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return got
+
+
+def _check(got, world, strategy, runs):
+    sys.path.insert(0, ROOT)
+    import oracle as O
+    from paper_2405_05329_b200 import kvprefill as kv
+    W = kv.init_weights(kv.ModelConfig(1024, 8, 2, 2, 5, "bf16", True), [0])
+    strat = kv.Strategy.KVR if strategy == "kvr" else kv.Strategy.TSP
+    for i, boundaries in enumerate(runs):
+        hidden = np.concatenate([got[r][i][0] for r in range(world)])
+        C_ = boundaries[-1]
+        ref = kv.run(kv.Strategy.Serial, O.random_context(C_, 1024, 11, np.float32), kv.even_partition(C_, 1), W)
+        assert np.array_equal(hidden, ref.hidden_out), (strategy, boundaries)
+        part = kv.ContextPartition(C_, boundaries)
+        m = got[0][i][1]
+        assert m["dot_products"] == [x * 2 for x in kv.dot_product_counts(strat, part)]
+        assert sum(m["kv_pairs_sent"]) == 2 * kv.traffic_pairs(strat, part)
+        assert sum(m["kv_pairs_received"]) == 2 * kv.traffic_pairs(strat, part)
 
 
 @pytest.mark.parametrize("strategy,boundaries", [("kvr", [0, 300, 517]), ("tsp", [0, 259, 517])])
 def test_two_processes_match_in_process_engine(strategy, boundaries):
-    sys.path.insert(0, ROOT)
-    import oracle as O
     from paper_2405_05329_b200 import kvprefill as kv
     if kv.device_count() == 0:
         pytest.skip("no CUDA device")
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, strategy, boundaries, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    got = {}
-    for _ in range(2):
-        rank, hidden, metrics = q.get(timeout=600)
-        got[rank] = (hidden, metrics)
-    for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
-    hidden = np.concatenate([got[0][0], got[1][0]])
-    W = kv.init_weights(kv.ModelConfig(1024, 8, 2, 2, 5, "bf16", True), [0])
-    C_ = boundaries[-1]
-    ref = kv.run(kv.Strategy.Serial, O.random_context(C_, 1024, 11, np.float32), kv.even_partition(C_, 1), W)
-    assert np.array_equal(hidden, ref.hidden_out)
-    strat = kv.Strategy.KVR if strategy == "kvr" else kv.Strategy.TSP
-    part = kv.ContextPartition(C_, boundaries)
-    assert got[0][1]["dot_products"] == [x * 2 for x in kv.dot_product_counts(strat, part)]
-    assert sum(got[0][1]["kv_pairs_sent"]) == 2 * kv.traffic_pairs(strat, part)
+    got = _run_procs(2, strategy, [boundaries], False)
+    _check(got, 2, strategy, [boundaries])
+
+
+@pytest.mark.parametrize("strategy,world,runs", [
+    ("kvr", 2, [[0, 300, 517], [0, 300, 517], [0, 100, 517]]),
+    ("kvr", 3, [[0, 200, 390, 517], [0, 200, 390, 517]]),
+    ("tsp", 3, [[0, 173, 345, 517], [0, 100, 345, 517]]),
+])
+def test_peer_memory_handoff_processes(strategy, world, runs):
+    """The fused handoff over peer memory (Transport(peer=True)): CUDA IPC mappings of the
+    other processes' caches, the QKV epilogue storing the K/V rows into them, stream-ordered
+    flags instead of messages, KVR prefix forwarded by the copy engine.  Several runs on one
+    executor (epoch-numbered flags, mappings re-opened when the partition changes); results
+    bitwise equal to the serial run, accounting equal to the reference's."""
+    from paper_2405_05329_b200 import kvprefill as kv
+    if kv.device_count() == 0:
+        pytest.skip("no CUDA device")
+    got = _run_procs(world, strategy, runs, True)
+    _check(got, world, strategy, runs)
 
 
 def test_bench_multi_rank_path_on_one_gpu():
@@ -82,7 +115,8 @@ def test_bench_multi_rank_path_on_one_gpu():
     import json
     import subprocess
     env = dict(os.environ, KVP_BENCH_SHARE_GPU="1", KVP_BENCH_BACKEND="gloo")
-    for i, extra in enumerate(([], ["--partition", "search"], ["--strategy", "tsp"])):
+    for i, extra in enumerate(([], ["--partition", "search"], ["--strategy", "tsp"], ["--transport", "msg"],
+                               ["--strategy", "tsp", "--transport", "msg"])):
         r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                             "--master-addr", "127.0.0.1", "--master-port", str(_port()),
                             os.path.join(ROOT, "bench.py"), "--gpus", "2", "--workload", "tiny", "--steps", "2",
