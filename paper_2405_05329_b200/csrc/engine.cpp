@@ -1212,6 +1212,7 @@ kvp_status kvp_engine_profile_layer(kvp_engine* e, int64_t rows, int64_t offset,
         const bool prof = R.profiling;
         R.profiling = false;
         for (int i = 0; i < reps + 1; ++i) {
+            launch_spin(300000, R.comp);  // device time only: the host enqueues behind the spin
             KVP_CUDA(cudaEventRecord(ev[0], R.comp));
             exec_qkv(s, w, R, rows, K + offset * row_kv, V + offset * row_kv, true);
             KVP_CUDA(cudaEventRecord(ev[1], R.comp));
@@ -1284,6 +1285,7 @@ kvp_status kvp_bench_gemm(kvp_engine* e, int64_t M, int64_t N, int64_t K, int32_
         KVP_CUDA(cudaEventCreate(&e1));
         std::vector<float> t;
         for (int i = 0; i < reps + 1; ++i) {
+            launch_spin(100000, st);  // device time only: the host enqueues behind the spin
             KVP_CUDA(cudaEventRecord(e0, st));
             gemm_bf16_tc(a.as<bf16>(), M, K, b.as<bf16>(), N, ep, st);
             KVP_CUDA(cudaEventRecord(e1, st));
@@ -1338,6 +1340,7 @@ kvp_status kvp_bench_attn(kvp_engine* e, int64_t q_rows, int64_t offset, int32_t
         KVP_CUDA(cudaEventCreate(&e1));
         std::vector<float> t;
         for (int i = 0; i < reps + 1; ++i) {
+            launch_spin(100000, st);  // device time only: the host enqueues behind the spin
             KVP_CUDA(cudaEventRecord(e0, st));
             attn_bf16(q.as<bf16>(), k.as<bf16>(), v.as<bf16>(), o.as<bf16>(), sh, st);
             KVP_CUDA(cudaEventRecord(e1, st));

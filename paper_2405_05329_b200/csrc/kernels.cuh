@@ -40,6 +40,8 @@ void launch_cast_bf16(const float* x, bf16* y, int64_t n, cudaStream_t s);
 // input of the fused-norm pipeline; later layers get both from the GEMM epilogues).
 void launch_prep_bf16_ssq(const float* x, bf16* y, float* ssq, int64_t rows, int64_t cols, cudaStream_t s);
 void launch_cast_f32(const bf16* x, float* y, int64_t n, cudaStream_t s);
+// timing helper (not counted as a product launch): keeps the stream busy for ns nanoseconds
+void launch_spin(uint64_t ns, cudaStream_t s);
 
 // ---------------------------------------------------------------- gemm_tc.cu
 // D = A[M x K] . B[N x K]^T on tcgen05 (bf16 in, f32 accumulate in TMEM), epilogue fused.

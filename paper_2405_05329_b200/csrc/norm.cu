@@ -128,4 +128,20 @@ void launch_cast_f32(const bf16* x, float* y, int64_t n, cudaStream_t s) {
     cast_f32_kernel<<<blocks_for(n, 256), 256, 0, s>>>(x, y, n);
 }
 
+// Timing helper: one thread spins on the global timer for ns nanoseconds, so the host can
+// enqueue the timed launches (tensor-map encodes, launch calls) while the stream is busy and
+// the events around them see device time only.
+__global__ void spin_kernel(uint64_t ns) {
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 >= ns) break;
+        __nanosleep(1000);
+    }
+}
+
+void launch_spin(uint64_t ns, cudaStream_t s) { spin_kernel<<<1, 32, 0, s>>>(ns); }
+
 }  // namespace kvp
