@@ -423,41 +423,60 @@ __global__ void __launch_bounds__(AD_WARPS * 32)
 // merge the segments of each (row, head) in segment order: one CTA of HD threads per
 // (row, head); the per-segment weights exp2(m_s - max) go through smem, then thread t sums
 // element t over the segments (independent, coalesced loads)
+constexpr int CB_G = 4;  // segment groups per output dimension in attn_decode_combine
+
 template <int HD>
-__global__ void __launch_bounds__(HD) attn_decode_combine(const float* part, int n_seg, int rows, int heads,
-                                                          int64_t ldo, bf16* O) {
-    extern __shared__ float wts[];  // [n_seg] weights, then [1] the sum of l
+__global__ void __launch_bounds__(HD * CB_G) attn_decode_combine(const float* part, int n_seg, int rows, int heads,
+                                                                 int64_t ldo, bf16* O) {
+    // Merges the segment partials (m, l, o[HD]) of one (row, head) in a FIXED order
+    // (deterministic): max and weights in parallel over segments, l by a fixed shuffle tree;
+    // thread (g, d) accumulates o[d] over segments s = g (mod CB_G) -- all of its loads
+    // independent and in flight at once -- and the CB_G group sums are added in order.
+    extern __shared__ float wts[];  // [n_seg] segment weights
     ptx::griddep_launch_dependents();
     ptx::griddep_wait();
+    constexpr int NT = HD * CB_G, NW = NT / 32;
     const int w = blockIdx.x, t = threadIdx.x;
     if (w >= rows * heads) return;
     const int i = w / heads, hq = w % heads;
     const float* base = part + static_cast<int64_t>(w) * n_seg * (HD + 2);
-    __shared__ float red[HD / 32];
+    __shared__ float red[NW], lred[NW];
+    __shared__ float po[CB_G - 1][HD];
     float mx = -INFINITY;
-    for (int s = t; s < n_seg; s += HD) mx = fmaxf(mx, base[s * (HD + 2)]);
+    for (int s = t; s < n_seg; s += NT) mx = fmaxf(mx, base[s * (HD + 2)]);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
     if ((t & 31) == 0) red[t >> 5] = mx;
     __syncthreads();
     mx = red[0];
 #pragma unroll
-    for (int q = 1; q < HD / 32; ++q) mx = fmaxf(mx, red[q]);
-    for (int s = t; s < n_seg; s += HD) {
+    for (int q = 1; q < NW; ++q) mx = fmaxf(mx, red[q]);
+    float lp = 0.f;
+    for (int s = t; s < n_seg; s += NT) {
         const float ms = base[s * (HD + 2)];
-        wts[s] = ms == -INFINITY ? 0.f : exp2f(ms - mx);  // a segment with no visible key weighs 0
+        const float wt = ms == -INFINITY ? 0.f : exp2f(ms - mx);  // a segment with no visible key weighs 0
+        wts[s] = wt;
+        lp = fmaf(base[s * (HD + 2) + 1], wt, lp);
     }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) lp += __shfl_xor_sync(0xffffffffu, lp, off);
+    if ((t & 31) == 0) lred[t >> 5] = lp;
     __syncthreads();
-    if (t == 0) {
-        float l = 0.f;
-        for (int s = 0; s < n_seg; ++s) l = fmaf(base[s * (HD + 2) + 1], wts[s], l);
-        wts[n_seg] = l;
-    }
+    const int d = t % HD, g = t / HD;
+    const float* col = base + 2 + d;
     float o = 0.f;
-#pragma unroll 8
-    for (int s = 0; s < n_seg; ++s) o = fmaf(base[s * (HD + 2) + 2 + t], wts[s], o);
+#pragma unroll 16
+    for (int s = g; s < n_seg; s += CB_G) o = fmaf(col[s * (HD + 2)], wts[s], o);
+    if (g > 0) po[g - 1][d] = o;
     __syncthreads();
-    O[i * ldo + static_cast<int64_t>(hq) * HD + t] = __float2bfloat16_rn(o / wts[n_seg]);
+    if (g == 0) {
+        float l = lred[0];
+#pragma unroll
+        for (int q = 1; q < NW; ++q) l += lred[q];
+#pragma unroll
+        for (int q = 0; q < CB_G - 1; ++q) o += po[q][d];
+        O[i * ldo + static_cast<int64_t>(hq) * HD + d] = __float2bfloat16_rn(o / l);
+    }
 }
 
 template <int HD>
@@ -482,8 +501,8 @@ void attn_decode_launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, co
     const int cw = static_cast<int>(sh.q_rows) * sh.n_heads;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(cw));
-    cfg.blockDim = dim3(HD);
-    cfg.dynamicSmemBytes = static_cast<size_t>(n_seg + 1) * 4;
+    cfg.blockDim = dim3(HD * CB_G);
+    cfg.dynamicSmemBytes = static_cast<size_t>(n_seg) * 4;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
