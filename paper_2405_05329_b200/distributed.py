@@ -263,7 +263,7 @@ class _PeerSession:
         torch = ex.torch
         torch.cuda.current_stream(ex.device).synchronize()
         mine = {"kv": _ipc_export(ex.kvbuf.data_ptr()), "rows": int(ex.kvbuf.shape[2]),
-                "flags": _ipc_export(self.flags.data_ptr()), "pid": __import__("os").getpid()}
+                "flags": _ipc_export(self.flags.data_ptr())}
         everyone = [None] * world
         dist.all_gather_object(everyone, mine, group=group)
         self.close()
