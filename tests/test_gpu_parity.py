@@ -355,3 +355,25 @@ def test_edge_partitions_bitwise(prec):
         if len(sizes) > 1 and len(set(sizes)) == 1:
             tsp = kv.run(kv.Strategy.TSP, ctx, kv.ContextPartition.from_sizes(sizes), W)
             assert np.array_equal(serial.hidden_out, tsp.hidden_out)
+
+
+# ------------------------------------------------------------ fused KV handoff (bf16)
+@pytest.mark.parametrize("kvh", [8, 2, 1])
+def test_fused_handoff_many_ranks_bitwise(kvh):
+    """bf16 KVR / TSP with the handoff fused into the QKV epilogue (KVR: one mirror per rank,
+    TSP: p - 1 mirrors, up to 8) and TSP at p = 9 (more receivers than mirror slots: the
+    copy-engine path) -- all bitwise equal to the serial run, accounting as the reference's."""
+    W = engine(512, 8, kvh, 2, 9, "bf16", True)
+    C_ = 777
+    ctx = O.random_context(C_, 512, 31, np.float32)
+    serial = kv.run(kv.Strategy.Serial, ctx, kv.even_partition(C_, 1), W)
+    den = 8 * 9 / 2
+    cases = [(kv.Strategy.KVR, kv.partition_from_ratios(C_, [(8 - i) / den for i in range(8)])),
+             (kv.Strategy.KVR, kv.even_partition(C_, 5)),
+             (kv.Strategy.TSP, kv.even_partition(C_, 9)),
+             (kv.Strategy.TSP, kv.partition_from_ratios(C_, [0.3, 0.1, 0.2, 0.1, 0.05, 0.05, 0.1, 0.1]))]
+    for strat, part in cases:
+        r = kv.run(strat, ctx, part, W)
+        assert np.array_equal(r.hidden_out, serial.hidden_out), (strat, part.boundaries)
+        assert r.metrics.dot_products == [x * 2 for x in kv.dot_product_counts(strat, part)]
+        assert r.metrics.total_pairs_sent() == kv.traffic_pairs(strat, part) * 2
