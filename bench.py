@@ -274,6 +274,50 @@ def kv_handoff_bandwidth(b, w, rank, world, local, reps=10):
     return out[0]
 
 
+def kv_handoff_bandwidth_peer(b, w, rank, world, ex, reps=10):
+    """The busiest KV-Runahead link (rank p-2 -> p-1, K and V rows [0, b_{p-1}) per layer) as
+    a peer-memory copy into rank p-1's IPC-mapped cache -- the copy the fused handoff's prefix
+    forward issues -- device-timed with CUDA events on the sender's stream, against 900 GB/s."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_05329_b200 import kvprefill as kv
+    ps = ex.peer
+    src, dst = world - 2, world - 1
+    kv_dim = w["n_kv_heads"] * (w["d_model"] // w["n_heads"])
+    rows = b[world - 1]
+    nbytes = 2 * rows * kv_dim * 2
+    times = []
+    for i in range(reps + 2):
+        dist.barrier()
+        if rank == src:
+            st = torch.cuda.current_stream()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            K, V = ex.kv(0)
+            peer_kv = ps.peers[dst]["kv"]
+            e0.record(st)
+            for plane, t in ((0, K), (1, V)):
+                kv._check(kv.lib().kvp_stream_copy(C.c_void_p(st.cuda_stream), C.c_void_p(peer_kv[plane]),
+                                                   C.c_void_p(t.data_ptr()), nbytes // 2), "stream_copy")
+            e1.record(st)
+            torch.cuda.synchronize()
+            if i >= 2:
+                times.append(e0.elapsed_time(e1))
+        dist.barrier()
+    out = [None]
+    if rank == src:
+        ms = statistics.median(times)
+        out = [{"link": f"{src}->{dst}", "bytes_per_layer": nbytes, "ms": ms, "gbs": nbytes / (ms * 1e-3) / 1e9,
+                "peak_gbs": 900.0, "frac": nbytes / (ms * 1e-3) / 1e9 / 900.0,
+                "note": "busiest link, isolated copy-engine copy into the receiver's IPC-mapped cache "
+                        "(the fused handoff's prefix forward); in the prefill it overlaps compute",
+                "same_gpu": os.environ.get("KVP_BENCH_SHARE_GPU") == "1"}]  # test hook: HBM, not NVLink
+    dist.broadcast_object_list(out, src=src)
+    return out[0]
+
+
 def run_multi(args, w, rank, world, local):
     """One process per GPU: KVR chain / TSP all-gather over NCCL through the distributed driver."""
     import torch
@@ -343,7 +387,10 @@ def run_multi(args, w, rank, world, local):
     handoff = None
     if strategy == kv.Strategy.KVR and world > 1:
         try:
-            handoff = kv_handoff_bandwidth(b, w, rank, world, local)
+            if ex.peer is not None:
+                handoff = kv_handoff_bandwidth_peer(b, w, rank, world, ex)
+            else:
+                handoff = kv_handoff_bandwidth(b, w, rank, world, local)
         except Exception as ex:  # the measurement must never break the bench line
             handoff = {"error": str(ex)}
     W.set_profiling(True)
