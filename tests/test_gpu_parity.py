@@ -377,3 +377,29 @@ def test_fused_handoff_many_ranks_bitwise(kvh):
         assert np.array_equal(r.hidden_out, serial.hidden_out), (strat, part.boundaries)
         assert r.metrics.dot_products == [x * 2 for x in kv.dot_product_counts(strat, part)]
         assert r.metrics.total_pairs_sent() == kv.traffic_pairs(strat, part) * 2
+
+
+def test_stream_signal_wait_copy_and_ipc_export():
+    """The peer-transport primitives of the C-ABI: a stream-ordered flag write releases a
+    stream waiting on it (GEQ), the async copy lands, and an IPC export of an interior pointer
+    reports its offset inside the allocation."""
+    import ctypes as C
+
+    import torch
+    lib = kv.lib()
+    flag = torch.zeros(4, dtype=torch.int32, device="cuda")
+    src = torch.arange(1 << 16, dtype=torch.float32, device="cuda")
+    dst = torch.zeros_like(src)
+    a, b = torch.cuda.Stream(), torch.cuda.Stream()
+    kv._check(lib.kvp_stream_wait(C.c_void_p(b.cuda_stream), C.c_void_p(flag.data_ptr() + 4), 7), "wait")
+    kv._check(lib.kvp_stream_copy(C.c_void_p(b.cuda_stream), C.c_void_p(dst.data_ptr()), C.c_void_p(src.data_ptr()),
+                                  src.numel() * 4), "copy")
+    kv._check(lib.kvp_stream_signal(C.c_void_p(a.cuda_stream), C.c_void_p(flag.data_ptr() + 4), 9), "signal")
+    b.synchronize()
+    assert torch.equal(dst, src) and int(flag[1]) == 9
+    h = (C.c_ubyte * 64)()
+    off = C.c_int64()
+    kv._check(lib.kvp_ipc_export(C.c_void_p(src.data_ptr() + 4096), h, C.byref(off)), "export")
+    off2 = C.c_int64()
+    kv._check(lib.kvp_ipc_export(C.c_void_p(src.data_ptr()), h, C.byref(off2)), "export")
+    assert off.value - off2.value == 4096
