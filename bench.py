@@ -533,7 +533,8 @@ def main():
     g_fl = sum(v["flops"] for v in gemm)
     roofline = {"bound": "tensor", "kernel": f"{dom_name} ({'tcgen05 GEMM' if dom_name.startswith('gemm') else 'tcgen05 attention'})",
                 "achieved": achieved, "peak": peaks["bf16_sustained"], "unit": "TFLOP/s",
-                "frac": achieved / peaks["bf16_sustained"], "traffic": traffic,
+                "frac": achieved / peaks["bf16_sustained"], "frac_of_burst": achieved / peaks["bf16"],
+                "traffic": traffic,
                 "peak_source": f"{peaks['source']} bf16_tflops_sustained (burst {peaks['bf16']})",
                 "flops_per_launch": dom_flops, "avg_launch_ms": dom_launch_ms,
                 "share_of_step": dom["total_ms"] / ms if ms else None,
