@@ -91,6 +91,10 @@ struct Cfg {
     static constexpr uint32_t smem_for(int kind) { return SMEM + (kind == EPI_RESID ? STAGING : 0); }
 };
 
+// EPI_QKV with the fused-handoff mirror stores (GemmEpilogue::n_mirror > 0): a separate
+// instantiation, so the plain QKV epilogue carries none of the mirror code
+constexpr int EPI_QKV_MIRROR = 4;
+
 struct EpiArgs {
     bf16* out0;
     int64_t ld0, n0;
@@ -122,7 +126,7 @@ __device__ __forceinline__ void store_chunk(const EpiArgs& ep, int64_t row, int6
         bf16* o;
         int region = 0;  // EPI_QKV: 1 = K, 2 = V chunk (also stored to the mirrors)
         int64_t region_off = 0;
-        if constexpr (KIND == EPI_QKV) {
+        if constexpr (KIND == EPI_QKV || KIND == EPI_QKV_MIRROR) {
             // chunks straddling the Q|K|V column boundaries (q or kv not a multiple of 32)
             // take the per-element path
             const int64_t e0 = ep.n0, e1 = ep.n0 + ep.n1;
@@ -135,10 +139,11 @@ __device__ __forceinline__ void store_chunk(const EpiArgs& ep, int64_t row, int6
                                        : (c < e1 ? ep.out1 + row * ep.ld1 + (c - e0) : ep.out2 + row * ep.ld2 + (c - e1));
                     const bf16 val = __float2bfloat16_rn(__uint_as_float(r[j]) * row_scale);
                     *dst = val;
+                    if constexpr (KIND == EPI_QKV_MIRROR)
 #pragma unroll
-                    for (int m = 0; m < 8; ++m)
-                        if (m < ep.n_mirror && c >= e0)
-                            *(c < e1 ? ep.mk[m] + row * ep.ld1 + (c - e0) : ep.mv[m] + row * ep.ld2 + (c - e1)) = val;
+                        for (int m = 0; m < 8; ++m)
+                            if (m < ep.n_mirror && c >= e0)
+                                *(c < e1 ? ep.mk[m] + row * ep.ld1 + (c - e0) : ep.mv[m] + row * ep.ld2 + (c - e1)) = val;
                 }
                 return;
             }
@@ -171,7 +176,7 @@ __device__ __forceinline__ void store_chunk(const EpiArgs& ep, int64_t row, int6
                 pk.z = ptx::pack_bf16(v[j + 4], v[j + 5]);
                 pk.w = ptx::pack_bf16(v[j + 6], v[j + 7]);
                 *reinterpret_cast<uint4*>(o + j) = pk;
-                if constexpr (KIND == EPI_QKV)
+                if constexpr (KIND == EPI_QKV_MIRROR)
 #pragma unroll
                     for (int m = 0; m < 8; ++m)
                         if (region && m < ep.n_mirror)
@@ -182,7 +187,7 @@ __device__ __forceinline__ void store_chunk(const EpiArgs& ep, int64_t row, int6
             for (int j = 0; j < 32; ++j)
                 if (col0 + j < N) {
                     o[j] = __float2bfloat16_rn(v[j]);
-                    if constexpr (KIND == EPI_QKV)
+                    if constexpr (KIND == EPI_QKV_MIRROR)
 #pragma unroll
                         for (int m = 0; m < 8; ++m)
                             if (region && m < ep.n_mirror) (region == 1 ? ep.mk[m] : ep.mv[m])[region_off + j] = o[j];
@@ -608,7 +613,12 @@ void dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
         ep.mv[m] = g.mirror_v[m];
     }
     switch (g.kind) {
-        case EPI_QKV: launch_tc<BN, EPI_QKV, NCTA>(ta, tb, tbh, M, N, K, ep, s); break;
+        case EPI_QKV:
+            if (ep.n_mirror > 0)
+                launch_tc<BN, EPI_QKV_MIRROR, NCTA>(ta, tb, tbh, M, N, K, ep, s);
+            else
+                launch_tc<BN, EPI_QKV, NCTA>(ta, tb, tbh, M, N, K, ep, s);
+            break;
         case EPI_RESID: launch_tc<BN, EPI_RESID, NCTA>(ta, tb, tbh, M, N, K, ep, s); break;
         case EPI_RELU: launch_tc<BN, EPI_RELU, NCTA>(ta, tb, tbh, M, N, K, ep, s); break;
         default: launch_tc<BN, EPI_STORE, NCTA>(ta, tb, tbh, M, N, K, ep, s); break;
