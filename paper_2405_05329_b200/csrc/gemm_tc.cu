@@ -213,7 +213,9 @@ __device__ __forceinline__ void resid_fetch(const EpiArgs& ep, const ResidT& t, 
         const int64_t row = t.row0 + t.rsub + 4 * i;
         const int64_t col = col0 + 4 * t.cg;
         if (full) {
-            rv[i] = *reinterpret_cast<const float4*>(ep.resid + row * ep.ldr + col);
+            // read once: evict-first, so the residual stream does not push the operand tiles
+            // out of L2
+            rv[i] = __ldcs(reinterpret_cast<const float4*>(ep.resid + row * ep.ldr + col));
         } else {
             float e[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -252,7 +254,9 @@ __device__ __forceinline__ void resid_store(const EpiArgs& ep, const ResidT& t, 
         v.w = rv[i].w + a.w;
         const int64_t row = t.row0 + rr, col = col0 + 4 * t.cg;
         if (full) {
-            *reinterpret_cast<float4*>(ep.outf + row * ep.ldf + col) = v;
+            // the f32 residual is next read layers/kernels later: streaming store; the bf16
+            // copy (the next GEMM's A operand) keeps the default policy
+            __stcs(reinterpret_cast<float4*>(ep.outf + row * ep.ldf + col), v);
             if (ep.outb) {
                 uint2 pk;
                 pk.x = ptx::pack_bf16(v.x, v.y);
