@@ -403,3 +403,24 @@ def test_stream_signal_wait_copy_and_ipc_export():
     off2 = C.c_int64()
     kv._check(lib.kvp_ipc_export(C.c_void_p(src.data_ptr()), h, C.byref(off2)), "export")
     assert off.value - off2.value == 4096
+
+
+def test_fused_handoff_random_configs_bitwise():
+    """Seeded random shapes / partitions through the fused bf16 handoff: every strategy and
+    partition gives the serial run's hidden states bit for bit."""
+    rng = np.random.default_rng(2405)
+    for trial in range(6):
+        d = int(rng.choice([256, 512, 1024]))
+        h = int(rng.choice([4, 8]))
+        kvh = int(rng.choice([x for x in (1, 2, 4, 8) if h % x == 0]))
+        W = engine(d, h, kvh, 2, 100 + trial, "bf16", bool(trial % 2))
+        p = int(rng.integers(2, 9))
+        C_ = int(rng.integers(2 * p, 600))
+        ctx = O.random_context(C_, d, 500 + trial, np.float32)
+        serial = kv.run(kv.Strategy.Serial, ctx, kv.even_partition(C_, 1), W)
+        raw = rng.uniform(0.2, 1.0, p)
+        part = kv.partition_from_ratios(C_, list(raw / raw.sum()))
+        for strat in (kv.Strategy.KVR, kv.Strategy.TSP):
+            r = kv.run(strat, ctx, part, W)
+            assert np.array_equal(r.hidden_out, serial.hidden_out), (trial, d, h, kvh, p, C_, strat)
+        W.close()
