@@ -194,6 +194,13 @@ class GpuExecutor:
         kv._check(kv.lib().kvp_rank_end(self.w.handle, C.c_void_p(out.ctypes.data), 0, None, C.byref(ms)), "rank_end")
         return out, float(ms.value)
 
+    def close(self):
+        """Releases the IPC mappings of the peer transport (the caches themselves are torch
+        tensors and go with the executor)."""
+        if self.peer is not None:
+            self.peer.close()
+            self.peer = None
+
     def raw_stream(self) -> int:
         return self._stream.cuda_stream
 
