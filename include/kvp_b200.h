@@ -116,6 +116,11 @@ kvp_status kvp_engine_destroy(kvp_engine* e);
 kvp_status kvp_engine_run(kvp_engine* e, int32_t strategy, const float* context, int64_t C,
                           const int64_t* boundaries, int64_t p, const kvp_fault* fault,
                           float* hidden_out, float* first_token, kvp_metrics* metrics);
+/* forward_serial (model.hpp:197-211): the single-rank prompt phase.  hidden_out (nullable):
+ * C x d.  kv_out (nullable): the per-layer KVCacheSegment{layer, 0, C, K, V} rows
+ * (kv_cache.hpp:14-31) as [n_layers][2][C][kv] f32, K before V. */
+kvp_status kvp_forward_serial(kvp_engine* e, const float* context, int64_t C, float* hidden_out,
+                              float* kv_out);
 /* Same, but context / hidden_out / first_token are device pointers on devices[0]
  * (inputs already resident in HBM). */
 kvp_status kvp_engine_run_device(kvp_engine* e, int32_t strategy, const float* context_dev,
@@ -250,6 +255,15 @@ kvp_status kvp_causal_attention(kvp_engine* e, const float* Q, int64_t q_rows, c
 kvp_status kvp_layer_finish(kvp_engine* e, int64_t layer, const float* hidden, int64_t rows,
                             const float* Q, const float* K, const float* V, int64_t k_rows,
                             int64_t offset, float* out);
+
+/* ------------------------------------------------ synthetic inputs */
+/* random_context<float>(rows, d_model, seed) (weights.hpp:86-89): uniform [-1, 1) from the
+ * SplitMix64 stream mix_seed(seed, 0xc7, 17) (rng.hpp:10-37), value = float((2u - 1) * 1.0)
+ * computed in double -- bit-identical to the reference.  Host: out is rows x d_model f32. */
+kvp_status kvp_random_context(int64_t rows, int64_t d_model, uint64_t seed, float* out);
+/* Same values generated on devices[0] of the engine into a device buffer (the counter
+ * generator runs one thread per element); synchronous. */
+kvp_status kvp_random_context_device(kvp_engine* e, int64_t rows, uint64_t seed, float* out_dev);
 
 /* ------------------------------------------------ partition plan (host) */
 kvp_status kvp_validate_partition(int64_t C, const int64_t* boundaries, int64_t p);

@@ -1,0 +1,5 @@
+// kvprefill/partition.hpp -- forwarding header so reference client code keeps its include line
+// (`#include "kvprefill/partition.hpp"`, reference proj/include/kvprefill/partition.hpp) and gets the
+// B200 drop-in: every name it declares lives in kvprefill_b200/kvprefill.hpp.
+#pragma once
+#include "../kvprefill_b200/kvprefill.hpp"

@@ -300,9 +300,45 @@ Matrix<T> random_context(int64_t rows, int64_t d_model, uint64_t seed) {
 }
 
 // ---------------------------------------------------------------- kv_cache.hpp / model.hpp
+// KVCacheSegment (kv_cache.hpp:14-31): K and V rows of one layer for token positions
+// [start_pos, end_pos); host copies of the device cache rows.
+template <typename T>
+struct KVCacheSegment {
+    int64_t layer = 0;
+    int64_t start_pos = 0;  // inclusive
+    int64_t end_pos = 0;    // exclusive
+    Matrix<T> K;
+    Matrix<T> V;
+
+    int64_t token_rows() const { return end_pos - start_pos; }
+
+    void validate() const {
+        if (start_pos < 0 || start_pos >= end_pos) throw CacheError("segment positions must satisfy 0 <= start < end");
+        if (K.rows != token_rows() || !K.same_shape(V))
+            throw CacheError("segment K/V rows must match the covered token range");
+    }
+};
+
 struct CausalMask {
     int64_t offset = 0, rows = 0;
 };
+
+// validate_cache_coverage (kv_cache.hpp:41-55): segments of one layer, gap-free from 0,
+// jointly covering [0, expected_tokens).
+template <typename T>
+void validate_cache_coverage(const std::vector<KVCacheSegment<T>>& segments, int64_t expected_tokens) {
+    int64_t next = 0;
+    for (const auto& seg : segments) {
+        seg.validate();
+        if (seg.start_pos != next)
+            throw CacheError("cache gap: expected segment at position " + std::to_string(next) + ", got " +
+                             std::to_string(seg.start_pos));
+        next = seg.end_pos;
+    }
+    if (next != expected_tokens)
+        throw CacheError("cache covers " + std::to_string(next) + " tokens, expected " +
+                         std::to_string(expected_tokens));
+}
 
 template <typename T>
 struct LayerQKV {
@@ -326,6 +362,15 @@ Matrix<T> causal_attention(const Matrix<T>& Q, const Matrix<T>& K, const Matrix<
                            const WeightSet<T>& w) {
     if (K.rows != V.rows || !K.same_shape(V)) throw DimensionError("causal_attention: K/V shape mismatch");
     if (Q.rows != mask.rows) throw DimensionError("causal_attention: Q rows != mask rows");
+    if (K.rows < mask.offset + Q.rows)
+        throw CacheError("causal_attention: cache holds " + std::to_string(K.rows) + " rows, need at least " +
+                         std::to_string(mask.offset + Q.rows));
+    // the reference indexes Q/K/V by head offsets (model.hpp:139-154); the C-ABI reads exactly
+    // q_dim / kv_dim columns per row, so narrower matrices are rejected here
+    if (Q.cols != w.config.q_dim() || K.cols != w.config.kv_dim())
+        throw DimensionError("causal_attention: Q/K/V widths " + std::to_string(Q.cols) + "/" + std::to_string(K.cols) +
+                             " != q_dim/kv_dim " + std::to_string(w.config.q_dim()) + "/" +
+                             std::to_string(w.config.kv_dim()));
     Matrix<T> A(Q.rows, w.config.q_dim());
     detail::check(kvp_causal_attention(w.engine(), Q.values.data(), Q.rows, K.values.data(), V.values.data(), K.rows,
                                        mask.offset, A.values.data()),
@@ -336,7 +381,17 @@ Matrix<T> causal_attention(const Matrix<T>& Q, const Matrix<T>& K, const Matrix<
 template <typename T>
 Matrix<T> layer_finish(const Matrix<T>& hidden, const Matrix<T>& Q, const Matrix<T>& K_full, const Matrix<T>& V_full,
                        int64_t offset, const WeightSet<T>& w, int64_t layer) {
+    const ModelConfig& c = w.config;
     if (!K_full.same_shape(V_full)) throw DimensionError("causal_attention: K/V shape mismatch");
+    if (Q.rows != hidden.rows) throw DimensionError("causal_attention: Q rows != mask rows");
+    if (K_full.rows < offset + Q.rows)
+        throw CacheError("causal_attention: cache holds " + std::to_string(K_full.rows) + " rows, need at least " +
+                         std::to_string(offset + Q.rows));
+    if (hidden.cols != c.d_model) throw DimensionError("add shape mismatch");
+    if (Q.cols != c.q_dim() || K_full.cols != c.kv_dim())
+        throw DimensionError("causal_attention: Q/K/V widths " + std::to_string(Q.cols) + "/" +
+                             std::to_string(K_full.cols) + " != q_dim/kv_dim " + std::to_string(c.q_dim()) + "/" +
+                             std::to_string(c.kv_dim()));
     Matrix<T> out(hidden.rows, w.config.d_model);
     detail::check(kvp_layer_finish(w.engine(), layer, hidden.values.data(), hidden.rows, Q.values.data(),
                                    K_full.values.data(), V_full.values.data(), K_full.rows, offset, out.values.data()),
@@ -400,6 +455,9 @@ ExecutionResult<T> run(Strategy strategy, const Matrix<T>& context, const Contex
         throw InputError("partition covers " + std::to_string(partition.context_length) +
                          " tokens but the context has " + std::to_string(context.rows) + " rows");
     const int64_t d = weights.config.d_model, C = context.rows, p = partition.process_count();
+    if (context.cols != d)  // qkv_project (model.hpp:68-70)
+        throw DimensionError("qkv_project: hidden width " + std::to_string(context.cols) + " != d_model " +
+                             std::to_string(d));
     ExecutionResult<T> r;
     r.hidden_out = Matrix<T>(C, d);
     r.first_token_hidden = Matrix<T>(1, d);
@@ -418,7 +476,34 @@ ExecutionResult<T> run(Strategy strategy, const Matrix<T>& context, const Contex
     return r;
 }
 
-// forward_serial (model.hpp:197-211): final hidden states (per-layer K/V stay on the GPU).
+// forward_serial (model.hpp:197-211): final hidden states (row C-1 is the first-token readout)
+// and one cache segment per layer covering [0, C), copied back from the device cache.
+template <typename T>
+std::pair<Matrix<T>, std::vector<KVCacheSegment<T>>> forward_serial(const Matrix<T>& context,
+                                                                    const WeightSet<T>& weights) {
+    if (context.rows < 1) throw InputError("forward_serial: empty context");
+    const ModelConfig& c = weights.config;
+    if (context.cols != c.d_model)
+        throw DimensionError("qkv_project: hidden width " + std::to_string(context.cols) + " != d_model " +
+                             std::to_string(c.d_model));
+    const int64_t C = context.rows, kv = c.kv_dim();
+    Matrix<T> h(C, c.d_model);
+    std::vector<float> kvbuf(static_cast<size_t>(c.n_layers * 2 * C * kv));
+    detail::check(kvp_forward_serial(weights.engine(), context.values.data(), C, h.values.data(), kvbuf.data()),
+                  "forward_serial");
+    std::vector<KVCacheSegment<T>> cache;
+    cache.reserve(static_cast<size_t>(c.n_layers));
+    for (int64_t l = 0; l < c.n_layers; ++l) {
+        KVCacheSegment<T> seg{l, 0, C, Matrix<T>(C, kv), Matrix<T>(C, kv)};
+        const float* k = kvbuf.data() + (2 * l) * C * kv;
+        std::copy(k, k + C * kv, seg.K.values.begin());
+        std::copy(k + C * kv, k + 2 * C * kv, seg.V.values.begin());
+        cache.push_back(std::move(seg));
+    }
+    return {std::move(h), std::move(cache)};
+}
+
+// Hidden states only (no K/V copy back to the host).
 template <typename T>
 Matrix<T> forward_serial_hidden(const Matrix<T>& context, const WeightSet<T>& weights) {
     if (context.rows < 1) throw InputError("forward_serial: empty context");

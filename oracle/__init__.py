@@ -206,6 +206,27 @@ def forward_serial(m: Model, weights, context: np.ndarray, want_kv: bool = False
     return (out, kv) if want_kv else out
 
 
+_FAST = os.path.join(HERE, "_build", "libkvoracle_fast.so")
+
+
+def forward_fast_f32(m: Model, context: np.ndarray, want_hidden: bool = True):
+    """forward_serial (model.hpp:197-211) in f32 at benchmark sizes: the multi-threaded
+    restatement in kvp_oracle_fast.c (same arithmetic as the reference, bit for bit) ->
+    (hidden [C x d] or None, last row [d])."""
+    if not os.path.exists(_FAST):
+        build()
+    lib = C.CDLL(_FAST)
+    fn = lib.kvof_forward_f32
+    fn.argtypes = [C.POINTER(_Config), C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+    ctx = np.ascontiguousarray(context, dtype=np.float32)
+    Cn = ctx.shape[0]
+    hid = np.empty((Cn, m.d_model), np.float32) if want_hidden else None
+    last = np.empty(m.d_model, np.float32)
+    cfg = m.c()
+    _check(fn(C.byref(cfg), _ptr(ctx), Cn, _ptr(hid) if want_hidden else None, _ptr(last)), "forward_fast")
+    return hid, last
+
+
 def naive_forward(m: Model, weights, context: np.ndarray) -> np.ndarray:
     """naive_causal_forward (oracle.hpp:34-111), f64."""
     fn = _Lib.get().kvo_naive_forward_f64

@@ -674,9 +674,15 @@ static void run_engine(kvp_engine* e, int32_t strategy, const float* ctx, int64_
         const int64_t held = (strategy == KVP_KVR) ? b[r + 1] : C;
         R.alloc(s, c, held);
         R.profiling = e->profiling;
+        // a rank session (kvp_rank_begin / KVCache.decode) may have left rank 0 in decode
+        // mode or holding peer mirrors: the prefill engine owns neither
+        R.decode = false;
+        R.n_mirror = 0;
+        R.mirror_bufs.clear();
         R.marks.clear();
         R.pool_used = 0;
     }
+    e->in_session = false;
 
     // Fused KV handoff (bf16): the QKV epilogue stores the rank's K/V rows straight into the
     // receiving ranks' layer buffers (peer memory over NVLink between GPUs), so the transfer
@@ -753,16 +759,25 @@ static void run_engine(kvp_engine* e, int32_t strategy, const float* ctx, int64_
                 const int64_t l0 = launch_count();
                 cudaGraph_t g = nullptr;
                 KVP_CUDA(cudaStreamBeginCapture(R.comp, cudaStreamCaptureModeThreadLocal));
-                for (int64_t l = 0; l < s.L; ++l) {
-                    const LayerW& w = e->weights[static_cast<size_t>(slot)]->layers[static_cast<size_t>(l)];
-                    uint8_t* K = static_cast<uint8_t*>(R.kv_ptr(s, l, 0));
-                    uint8_t* V = static_cast<uint8_t*>(R.kv_ptr(s, l, 1));
-                    KVP_CUDA(cudaEventRecord(R.t_start[l], R.comp));
-                    exec_qkv(s, w, R, c, K, V, l == 0);
-                    KVP_CUDA(cudaEventRecord(R.t_qkv[l], R.comp));
-                    KVP_CUDA(cudaEventRecord(R.t_attn[l], R.comp));
-                    exec_finish(s, w, R, c, K, V, c, 0);
-                    KVP_CUDA(cudaEventRecord(R.t_end[l], R.comp));
+                try {
+                    for (int64_t l = 0; l < s.L; ++l) {
+                        const LayerW& w = e->weights[static_cast<size_t>(slot)]->layers[static_cast<size_t>(l)];
+                        uint8_t* K = static_cast<uint8_t*>(R.kv_ptr(s, l, 0));
+                        uint8_t* V = static_cast<uint8_t*>(R.kv_ptr(s, l, 1));
+                        KVP_CUDA(cudaEventRecord(R.t_start[l], R.comp));
+                        exec_qkv(s, w, R, c, K, V, l == 0);
+                        KVP_CUDA(cudaEventRecord(R.t_qkv[l], R.comp));
+                        KVP_CUDA(cudaEventRecord(R.t_attn[l], R.comp));
+                        exec_finish(s, w, R, c, K, V, c, 0);
+                        KVP_CUDA(cudaEventRecord(R.t_end[l], R.comp));
+                    }
+                } catch (...) {
+                    // never leave the stream in capture mode: later runs would all fail
+                    cudaGraph_t dead = nullptr;
+                    cudaStreamEndCapture(R.comp, &dead);
+                    if (dead) cudaGraphDestroy(dead);
+                    cudaGetLastError();
+                    throw;
                 }
                 KVP_CUDA(cudaStreamEndCapture(R.comp, &g));
                 KVP_CUDA(cudaGraphInstantiate(&R.graph, g, 0));
@@ -1078,6 +1093,20 @@ kvp_status kvp_engine_load_layer(kvp_engine* e, int64_t layer, const float* wq, 
     });
 }
 
+// random_context<float> (weights.hpp:86-89) generated on devices[0]: same stream and values
+// as the host kvp_random_context (SplitMix64 is a counter generator).
+kvp_status kvp_random_context_device(kvp_engine* e, int64_t rows, uint64_t seed, float* out_dev) {
+    return guard([&] {
+        if (!e || !out_dev) throw Error(KVP_ERR_INPUT, "null argument");
+        if (rows < 0) throw Error(KVP_ERR_DIMENSION, "matrix dimensions must be non-negative");
+        std::lock_guard<std::mutex> g(e->mu);
+        KVP_CUDA(cudaSetDevice(e->devices[0]));
+        if (rows > 0) launch_seeded_f32(out_dev, rows, e->s.d, 1.0, mix_seed(seed, 0xc7u, 17), nullptr);
+        KVP_CUDA(cudaGetLastError());
+        KVP_CUDA(cudaDeviceSynchronize());
+    });
+}
+
 kvp_status kvp_engine_destroy(kvp_engine* e) {
     return guard([&] {
         if (!e) return;
@@ -1099,6 +1128,29 @@ kvp_status kvp_engine_run(kvp_engine* e, int32_t strategy, const float* context,
         if (!e) throw Error(KVP_ERR_INPUT, "null engine");
         std::lock_guard<std::mutex> g(e->mu);
         run_engine(e, strategy, context, C, boundaries, p, fault, hidden_out, first_token, metrics);
+    });
+}
+
+// forward_serial (model.hpp:197-211): the p = 1 prompt phase, plus one KVCacheSegment per
+// layer covering [0, C) (kv_cache.hpp:14-31): kv_out is [L][2][C][kv] f32 (K then V).
+kvp_status kvp_forward_serial(kvp_engine* e, const float* context, int64_t C, float* hidden_out, float* kv_out) {
+    return guard([&] {
+        if (!e) throw Error(KVP_ERR_INPUT, "null engine");
+        if (C < 1) throw Error(KVP_ERR_INPUT, "forward_serial: empty context");
+        std::lock_guard<std::mutex> g(e->mu);
+        const int64_t b[2] = {0, C};
+        run_engine(e, KVP_SERIAL, context, C, b, 1, nullptr, hidden_out, nullptr, nullptr);
+        if (!kv_out) return;
+        const Shape& s = e->s;
+        RankCtx& R = *e->ranks[0];
+        KVP_CUDA(cudaSetDevice(R.device));
+        DevBuf tmp;
+        if (s.prec != KVP_F32) tmp.ensure(static_cast<size_t>(C) * s.kv * 4, R.device);
+        for (int64_t l = 0; l < s.L; ++l)
+            for (int which = 0; which < 2; ++which) {
+                download_elems(s, kv_out + (2 * l + which) * C * s.kv, R.kv_ptr(s, l, which), C * s.kv, tmp, R.comp);
+                KVP_CUDA(cudaStreamSynchronize(R.comp));
+            }
     });
 }
 

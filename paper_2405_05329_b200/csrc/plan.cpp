@@ -647,3 +647,25 @@ kvp_status kvp_fit_cost_model(const int64_t* local_rows, const int64_t* held_row
 }
 
 }  // extern "C"
+
+// random_context<float> (weights.hpp:86-89) on the host: stream mix_seed(seed, 0xc7, 17),
+// value = float((2u - 1) * 1.0) in double, row-major fill (weights.hpp:41-47).
+kvp_status kvp_random_context(int64_t rows, int64_t d_model, uint64_t seed, float* out) {
+    return kvp::guard([&] {
+        if (rows < 0 || d_model < 0) throw kvp::Error(KVP_ERR_DIMENSION, "matrix dimensions must be non-negative");
+        if (!out && rows * d_model > 0) throw kvp::Error(KVP_ERR_INPUT, "null output");
+        auto next = [](uint64_t& st) {
+            uint64_t z = (st += 0x9e3779b97f4a7c15ULL);
+            z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+            z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+            return z ^ (z >> 31);
+        };
+        uint64_t g = seed;  // mix_seed (rng.hpp:28-37)
+        uint64_t h = next(g) ^ (0xc7ULL * 0xd1342543de82ef95ULL);
+        uint64_t st = next(h) ^ (17ULL * 0xaf251af3b0f025b5ULL);
+        for (int64_t i = 0; i < rows * d_model; ++i) {
+            const double u = static_cast<double>(next(st) >> 11) * 0x1.0p-53;
+            out[i] = static_cast<float>((2.0 * u - 1.0) * 1.0);
+        }
+    });
+}

@@ -138,6 +138,9 @@ _SIGS = {
     "kvp_kv_cache_reset": (C.c_int, [_P, C.c_int64]),
     "kvp_prefill_cached": (C.c_int, [_P, _P, _P, C.c_int64, _P, _P, C.POINTER(C.c_float)]),
     "kvp_decode": (C.c_int, [_P, _P, _P, C.c_int64, _P, C.POINTER(C.c_float)]),
+    "kvp_forward_serial": (C.c_int, [_P, _P, C.c_int64, _P, _P]),
+    "kvp_random_context": (C.c_int, [C.c_int64, C.c_int64, C.c_uint64, _P]),
+    "kvp_random_context_device": (C.c_int, [_P, C.c_int64, C.c_uint64, _P]),
     "kvp_layer_qkv": (C.c_int, [_P, C.c_int64, _P, C.c_int64, _P, _P, _P]),
     "kvp_causal_attention": (C.c_int, [_P, _P, C.c_int64, _P, _P, C.c_int64, C.c_int64, _P]),
     "kvp_layer_finish": (C.c_int, [_P, C.c_int64, _P, C.c_int64, _P, _P, _P, C.c_int64, C.c_int64, _P]),
@@ -611,12 +614,67 @@ def layer_finish(hidden, Q, K_full, V_full, offset: int, weights: WeightSet, lay
     return out
 
 
-def forward_serial(context, weights: WeightSet) -> np.ndarray:
-    """forward_serial (model.hpp:197-211) -> final hidden states."""
+@dataclass
+class KVCacheSegment:
+    """KVCacheSegment (kv_cache.hpp:14-31): K and V rows of one layer for token positions
+    [start_pos, end_pos)."""
+    layer: int
+    start_pos: int
+    end_pos: int
+    K: np.ndarray
+    V: np.ndarray
+
+    def token_rows(self) -> int:
+        return self.end_pos - self.start_pos
+
+    def validate(self) -> None:
+        if self.start_pos < 0 or self.start_pos >= self.end_pos:
+            raise CacheError("segment positions must satisfy 0 <= start < end")
+        if self.K.shape[0] != self.token_rows() or self.K.shape != self.V.shape:
+            raise CacheError("segment K/V rows must match the covered token range")
+
+
+def validate_cache_coverage(segments: Sequence[KVCacheSegment], expected_tokens: int) -> None:
+    """validate_cache_coverage (kv_cache.hpp:41-55)."""
+    nxt = 0
+    for seg in segments:
+        seg.validate()
+        if seg.start_pos != nxt:
+            raise CacheError(f"cache gap: expected segment at position {nxt}, got {seg.start_pos}")
+        nxt = seg.end_pos
+    if nxt != expected_tokens:
+        raise CacheError(f"cache covers {nxt} tokens, expected {expected_tokens}")
+
+
+def forward_serial(context, weights: WeightSet):
+    """forward_serial (model.hpp:197-211) -> (final hidden states [C x d], one KVCacheSegment
+    per layer covering [0, C), copied back from the device cache)."""
     ctx = _f32(context)
-    if ctx.shape[0] < 1:
+    if ctx.ndim != 2 or ctx.shape[0] < 1:
         raise InputError("forward_serial: empty context")
-    return run(Strategy.Serial, ctx, even_partition(ctx.shape[0], 1), weights).hidden_out
+    cfg = weights.config
+    if ctx.shape[1] != cfg.d_model:
+        raise DimensionError(f"qkv_project: hidden width {ctx.shape[1]} != d_model {cfg.d_model}")
+    Cn = ctx.shape[0]
+    hid = np.empty((Cn, cfg.d_model), np.float32)
+    kvb = np.empty((cfg.n_layers, 2, Cn, cfg.kv_dim()), np.float32)
+    _check(lib().kvp_forward_serial(weights.handle, _vp(ctx), Cn, _vp(hid), _vp(kvb)), "forward_serial")
+    return hid, [KVCacheSegment(l, 0, Cn, kvb[l, 0], kvb[l, 1]) for l in range(cfg.n_layers)]
+
+
+def random_context(rows: int, d_model: int, seed: int) -> np.ndarray:
+    """random_context<float> (weights.hpp:86-89): rows x d_model uniform [-1, 1) from the
+    SplitMix64 stream mix_seed(seed, 0xc7, 17) -- the reference's prompt, bit for bit."""
+    out = np.empty((int(rows), int(d_model)), np.float32)
+    _check(lib().kvp_random_context(int(rows), int(d_model), int(seed), _vp(out)), "random_context")
+    return out
+
+
+def random_context_device(weights: WeightSet, rows: int, seed: int, out_ptr: int) -> None:
+    """random_context generated on the engine's first device into a [rows x d_model] f32
+    device buffer (same values as random_context)."""
+    _check(lib().kvp_random_context_device(weights.handle, int(rows), int(seed), C.c_void_p(out_ptr)),
+           "random_context_device")
 
 
 # ------------------------------------------------------------------ search.hpp / simnet.hpp

@@ -1,10 +1,11 @@
 // Drop-in check: reference-style client code (the shapes of test_engine.cpp / acceptance.cpp)
-// compiled against include/kvprefill_b200/kvprefill.hpp and linked to libkvp_b200.so.
+// compiled against the drop-in with the reference's own include line (include/kvprefill/ forwards
+// to include/kvprefill_b200/kvprefill.hpp) and linked to libkvp_b200.so.
 // Exit 0 = all checks passed; prints one line per check.
 #include <cstdio>
 #include <string>
 
-#include "kvprefill_b200/kvprefill.hpp"
+#include "kvprefill/kvprefill.hpp"
 
 using namespace kvprefill;
 
@@ -33,6 +34,26 @@ int main(int argc, char** argv) {
     sim.n_layers = 32;
     const auto found = search_partition(16384, 4, sim, CostModel{}, NetworkModel{});
     expect(found.partition.boundaries == std::vector<int64_t>({0, 6564, 10621, 13754, 16384}), "KVR-S search p=4 16k");
+    // kv_cache.hpp: segment validation and coverage (host types)
+    KVCacheSegment<float> s0{0, 0, 4, Matrix<float>(4, 8), Matrix<float>(4, 8)};
+    KVCacheSegment<float> s1{0, 4, 9, Matrix<float>(5, 8), Matrix<float>(5, 8)};
+    bool covered = true;
+    try {
+        validate_cache_coverage<float>({s0, s1}, 9);
+    } catch (const Error&) {
+        covered = false;
+    }
+    bool gap = false;
+    try {
+        validate_cache_coverage<float>({s1}, 9);
+    } catch (const CacheError&) {
+        gap = true;
+    }
+    expect(covered && gap, "validate_cache_coverage: gap-free accepted, gap -> CacheError");
+    // weights.hpp random_context: the reference's SplitMix64 prompt, host side
+    std::vector<float> via_abi(1024 * 32);
+    detail::check(kvp_random_context(1024, 32, 18, via_abi.data()), "random_context");
+    expect(random_context<float>(1024, 32, 18).values == via_abi, "random_context header == C-ABI");
     if (!gpu) return failures ? 1 : 0;
 
     // device parts: the reference's accounting fixture and bitwise strategy equivalence
@@ -57,6 +78,27 @@ int main(int argc, char** argv) {
            "TSP 18 pairs / L barriers");
     const auto serial = run(Strategy::Serial, ctx, even_partition(9, 1), w);
     expect(serial.hidden_out == kvr.hidden_out && serial.hidden_out == tsp.hidden_out, "Serial == KVR == TSP bitwise");
+    // forward_serial (model.hpp:197-211): hidden states + one [0, C) segment per layer
+    const auto fs = forward_serial(ctx, w);
+    expect(fs.first == serial.hidden_out && fs.second.size() == 2, "forward_serial hidden == run(Serial)");
+    bool segs_ok = true;
+    for (const auto& seg : fs.second) {
+        try {
+            validate_cache_coverage<float>({seg}, 9);
+        } catch (const Error&) {
+            segs_ok = false;
+        }
+    }
+    const auto qkv0 = layer_qkv(ctx, w, 0);
+    expect(segs_ok && fs.second[0].K == qkv0.K && fs.second[0].V == qkv0.V,
+           "forward_serial segments cover [0, C); layer 0 K/V == layer_qkv (f32, bitwise)");
+    bool narrow = false;
+    try {
+        run(Strategy::Serial, Matrix<float>(9, 4), even_partition(9, 1), w);
+    } catch (const DimensionError&) {
+        narrow = true;
+    }
+    expect(narrow, "context width != d_model -> DimensionError");
     bool proto = false;
     try {
         FaultInjection f;

@@ -127,6 +127,29 @@ def test_bench_multi_rank_path_on_one_gpu():
         d = json.loads(lines[0])
         assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] > 0
         assert d["config"]["partition"][0] == 0 and d["config"]["partition"][-1] == 1024
+        if i == 0:  # the north-star comparison rides every N>1 line
+            t = d["strategies"]
+            assert {"kvr_even", "kvr_s", "tsp"} <= set(t) and t["kvr_s_over_tsp"] > 0
+            assert t["kvr_s"]["partition"][-1] == 1024 and len(d["kernels_per_rank"]) == 2
+            assert d["e2e"]["value"] > 0
+
+
+def test_bench_single_process_ranks_table():
+    """python bench.py --gpus 1 --ranks 4: the in-process engine with 4 ranks on one GPU; the
+    line carries KVR even / KVR-S / TSP TTFTs on the same kernels and the busiest link's
+    handoff copy, and the prompt's first token matches the reference's golden argmax."""
+    import json
+    import subprocess
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "1", "--ranks", "4", "--workload",
+                        "tiny", "--steps", "2", "--warmup", "3", "--partition", "search", "--no-cpu-baseline",
+                        "--no-decode"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    t = d["strategies"]
+    assert {"kvr_even", "kvr_s", "tsp"} <= set(t), t
+    assert d["config"]["ranks"] == 4 and len(d["config"]["partition"]) == 5
+    assert d["kv_handoff"]["bytes_per_layer"] > 0
+    assert d["first_token_matches_reference"] is True
 
 
 def _decode_worker(rank, world, port, outq):
