@@ -43,8 +43,8 @@ class Transport:
         """peer: move K/V through peer memory (CUDA IPC mappings of the other ranks' caches,
         NVLink between GPUs) instead of messages -- the QKV epilogue stores the rows straight
         into the receiver's cache and stream-ordered flags say they have landed; the group
-        then only carries host metadata.  Default: KVP_TRANSPORT=peer (explicit opt-out:
-        KVP_TRANSPORT=msg)."""
+        then only carries host metadata.  Default (peer=None): messages, unless the
+        environment says KVP_TRANSPORT=peer; bench.py passes peer=True explicitly."""
         import os
         import torch.distributed as dist
         self.dist = dist
@@ -70,9 +70,10 @@ class Transport:
         on_cuda = dev is not None and getattr(dev, "type", "cpu") == "cuda"
         return self.backend == "nccl" or not on_cuda
 
-    def all_gather_rows(self, buf, start: int, stop: int) -> None:
-        """buf[start:stop] of every rank into buf[0:C] (equal chunks, rank order)."""
-        self.dist.all_gather_into_tensor(buf, buf[start:stop].clone(), group=self.group)
+    def all_gather_rows(self, buf, start: int, stop: int, C_: int) -> None:
+        """buf[start:stop] of every rank into buf[0:C] (equal chunks, rank order).  The layer
+        plane may hold more rows (decode capacity): only the prompt's C rows are gathered."""
+        self.dist.all_gather_into_tensor(buf[:C_], buf[start:stop].clone(), group=self.group)
 
     def exchange(self, sends, recvs, wait: bool = True):
         """sends: [(tensor, dst)], recvs: [(tensor, src)] -- one batched group.  wait=False
@@ -196,7 +197,9 @@ class GpuExecutor:
 
     def close(self):
         """Releases the IPC mappings of the peer transport (the caches themselves are torch
-        tensors and go with the executor)."""
+        tensors and go with the executor).  Collective: every rank of the group closes (or
+        re-creates) its executor together, because the next peer run re-exchanges handles
+        with an all-gather that every rank must join."""
         if self.peer is not None:
             self.peer.close()
             self.peer = None
@@ -270,9 +273,13 @@ class _PeerSession:
         torch = ex.torch
         torch.cuda.current_stream(ex.device).synchronize()
         mine = {"kv": _ipc_export(ex.kvbuf.data_ptr()), "rows": int(ex.kvbuf.shape[2]),
-                "flags": _ipc_export(self.flags.data_ptr())}
+                "flags": _ipc_export(self.flags.data_ptr()), "epoch": self.epoch}
         everyone = [None] * world
         dist.all_gather_object(everyone, mine, group=group)
+        # every rank continues from the same epoch: a rank whose session is younger (its
+        # executor was re-created) must not wait on flag values another rank's earlier runs
+        # already wrote (GEQ waits would pass early)
+        self.epoch = max(info["epoch"] for info in everyone)
         self.close()
         L, kvd = ex.cfg.n_layers, ex.cfg.kv_dim()
         es = ex.kvbuf.element_size()
@@ -470,8 +477,8 @@ def run_rank(strategy: kv.Strategy, rows, partition: kv.ContextPartition, execut
                 # no fault can be injected and the chunks are equal: the all-gather is ONE
                 # collective per tensor (NCCL all-gather over NVLink/NVSwitch), in place in the
                 # [C x kv] layer buffer; the accounting is the reference's
-                transport.all_gather_rows(K, start, stop)
-                transport.all_gather_rows(V, start, stop)
+                transport.all_gather_rows(K, start, stop, C_)
+                transport.all_gather_rows(V, start, stop, C_)
                 for peer in range(p):
                     if peer != rank:
                         sent_ctr[0] += stop - start
