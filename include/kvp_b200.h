@@ -256,6 +256,14 @@ kvp_status kvp_layer_finish(kvp_engine* e, int64_t layer, const float* hidden, i
                             const float* Q, const float* K, const float* V, int64_t k_rows,
                             int64_t offset, float* out);
 
+/* Opt-in rotary position embedding (an extension: the reference model has no positional
+ * encoding, so it is OFF by default and unavailable in the f32 parity mode).  theta > 0
+ * enables it for bf16 engines with head_dim % 32 == 0: pairs (2i, 2i+1) of every Q and K
+ * head of the token at absolute position t rotate by t * theta^(-2i/head_dim), fused into the
+ * QKV projection epilogue (prefill, every strategy and rank, and decode); theta <= 0 disables.
+ * The per-op helpers (kvp_layer_qkv) never apply it. */
+kvp_status kvp_engine_set_rope(kvp_engine* e, double theta);
+
 /* ------------------------------------------------ synthetic inputs */
 /* random_context<float>(rows, d_model, seed) (weights.hpp:86-89): uniform [-1, 1) from the
  * SplitMix64 stream mix_seed(seed, 0xc7, 17) (rng.hpp:10-37), value = float((2u - 1) * 1.0)

@@ -276,6 +276,8 @@ class WeightSet {
         engine_.reset(e, [](kvp_engine* x) { kvp_engine_destroy(x); });
     }
     kvp_engine* engine() const { return engine_.get(); }
+    // Opt-in rotary position embedding (extension, bf16 only; kvp_engine_set_rope).
+    void set_rope(double theta) const { detail::check(kvp_engine_set_rope(engine_.get(), theta), "set_rope"); }
 
   private:
     std::shared_ptr<kvp_engine> engine_;

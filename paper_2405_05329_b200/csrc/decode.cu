@@ -182,6 +182,23 @@ __global__ void __launch_bounds__(GV_WARPS * 32) gemv_bf16_kernel(GvArgs g) {
                 scale = 1.0f / sqrtf(ss * g.inv_norm_cols + 1e-6f);
             }
         }
+        if constexpr (KIND == EPI_QKV) {
+            // opt-in rotary embedding of the Q and K columns (GemmEpilogue::rope_*): GV_COLS is
+            // even and n0 a multiple of it, so the column group holds whole (2i, 2i+1) pairs
+            if (ep.rope_hd > 0 && n0 < ep.n0 + ep.n1) {
+                const int64_t rc0 = n0 < ep.n0 ? n0 : n0 - ep.n0;
+                const float fpos = static_cast<float>(ep.rope_pos0 + r);
+#pragma unroll
+                for (int c = 0; c < GV_COLS; c += 2) {
+                    float sn, cs;
+                    sincosf(fpos * __ldg(ep.rope_inv_freq + ((rc0 + c) % ep.rope_hd) / 2), &sn, &cs);
+                    // the rotation is linear, so it commutes with the RMSNorm row scale
+                    const float x0 = acc[r][c], x1 = acc[r][c + 1];
+                    acc[r][c] = x0 * cs - x1 * sn;
+                    acc[r][c + 1] = x0 * sn + x1 * cs;
+                }
+            }
+        }
 #pragma unroll
         for (int c = 0; c < GV_COLS; ++c) {
             const int64_t n = n0 + c;

@@ -140,6 +140,7 @@ struct LayerW {
 struct DeviceWeights {
     int device = 0;
     DevBuf blob;
+    DevBuf rope;  // opt-in rotary embedding: inv_freq[head_dim / 2] (kvp_engine_set_rope)
     std::vector<LayerW> layers;
 
     void init(const Shape& s, int dev) {
@@ -341,6 +342,9 @@ struct RankCtx {
     std::vector<void*> mirror_bufs;  // multi-process fused handoff: [n_mirror][L][K,V] peer buffers
     int n_mirror = 0;
     bool decode = false;        // decode step: HBM-bound GEMV + split-key attention kernels
+    int64_t pos0 = 0;           // absolute position of this rank's first row (RoPE)
+    const float* rope_inv = nullptr;  // RoPE inv_freq table on this rank's device (nullptr: off)
+    int rope_hd = 0;
     DevBuf scratch;             // decode attention partials
     std::vector<cudaEvent_t> ev_send, ev_ready, t_start, t_qkv, t_attn, t_end;
     cudaEvent_t ev_begin = nullptr, ev_done = nullptr;
@@ -490,6 +494,11 @@ static void exec_qkv(const Shape& s, const LayerW& w, RankCtx& R, int64_t c, voi
                 ep.norm_src = R.h.as<float>();
                 ep.ld_norm = s.d;
             }
+        }
+        if (R.rope_inv) {
+            ep.rope_hd = static_cast<int>(s.hd);
+            ep.rope_pos0 = R.pos0;
+            ep.rope_inv_freq = R.rope_inv;
         }
         if (mir) {
             ep.n_mirror = mir->n;
@@ -642,6 +651,13 @@ struct kvp_engine {
     bool in_session = false;
     int64_t sess_rows = 0, sess_start = 0, sess_launch0 = 0;
     bool peer_ok = true;  // every device pair of this engine can address each other's memory
+    // opt-in rotary embedding (extension; 0 = off, the reference model): base theta and a
+    // generation counter that invalidates captured prefill graphs when it changes
+    double rope_theta = 0.0;
+    uint64_t rope_gen = 0;
+    const float* rope_table(int slot) const {
+        return rope_theta > 0 ? weights[static_cast<size_t>(slot)]->rope.as<float>() : nullptr;
+    }
 };
 
 namespace kvp {
@@ -674,6 +690,9 @@ static void run_engine(kvp_engine* e, int32_t strategy, const float* ctx, int64_
         const int64_t held = (strategy == KVP_KVR) ? b[r + 1] : C;
         R.alloc(s, c, held);
         R.profiling = e->profiling;
+        R.pos0 = b[r];
+        R.rope_inv = e->rope_table(static_cast<int>(r % nd));
+        R.rope_hd = R.rope_inv ? static_cast<int>(s.hd) : 0;
         // a rank session (kvp_rank_begin / KVCache.decode) may have left rank 0 in decode
         // mode or holding peer mirrors: the prefill engine owns neither
         R.decode = false;
@@ -752,7 +771,7 @@ static void run_engine(kvp_engine* e, int32_t strategy, const float* ctx, int64_
         if (p == 1 && strategy != KVP_TSP && use_graph && !R.profiling) {
             const uint64_t key = (static_cast<uint64_t>(c) << 20) ^ (reinterpret_cast<uintptr_t>(R.h.p) >> 4) ^
                                  (reinterpret_cast<uintptr_t>(R.kv.p) << 7) ^ (reinterpret_cast<uintptr_t>(R.x.p) << 13) ^
-                                 static_cast<uint64_t>(strategy);
+                                 static_cast<uint64_t>(strategy) ^ (e->rope_gen << 44);
             if (!R.graph || R.graph_key != key) {
                 if (R.graph) cudaGraphExecDestroy(R.graph);
                 R.graph = nullptr;
@@ -1093,6 +1112,34 @@ kvp_status kvp_engine_load_layer(kvp_engine* e, int64_t layer, const float* wq, 
     });
 }
 
+// Opt-in rotary position embedding (extension: the reference model has none).
+// Pairs (2i, 2i+1) of every Q and K head rotate by position * theta^(-2i/head_dim), applied in
+// the QKV projection's epilogue before the rows reach the KV cache (and the handoff mirrors).
+kvp_status kvp_engine_set_rope(kvp_engine* e, double theta) {
+    return guard([&] {
+        if (!e) throw Error(KVP_ERR_INPUT, "null engine");
+        std::lock_guard<std::mutex> g(e->mu);
+        const Shape& s = e->s;
+        if (theta > 0) {
+            if (s.prec != KVP_BF16)
+                throw Error(KVP_ERR_CONFIG, "RoPE is a bf16-mode extension; the f32 parity mode keeps the reference model");
+            if (s.hd % 32 != 0) throw Error(KVP_ERR_CONFIG, "RoPE needs head_dim to be a multiple of 32");
+            // inv_freq[i] = 1 / theta^(2i / head_dim) in f32 (the usual fp32 table)
+            std::vector<float> inv(static_cast<size_t>(s.hd / 2));
+            for (int64_t i = 0; i < s.hd / 2; ++i)
+                inv[static_cast<size_t>(i)] =
+                    1.0f / std::pow(static_cast<float>(theta), static_cast<float>(2 * i) / static_cast<float>(s.hd));
+            for (auto& w : e->weights) {
+                KVP_CUDA(cudaSetDevice(w->device));
+                w->rope.ensure(inv.size() * 4, w->device);
+                KVP_CUDA(cudaMemcpy(w->rope.p, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice));
+            }
+        }
+        e->rope_theta = theta > 0 ? theta : 0.0;
+        e->rope_gen += 1;
+    });
+}
+
 // random_context<float> (weights.hpp:86-89) generated on devices[0]: same stream and values
 // as the host kvp_random_context (SplitMix64 is a counter generator).
 kvp_status kvp_random_context_device(kvp_engine* e, int64_t rows, uint64_t seed, float* out_dev) {
@@ -1423,6 +1470,9 @@ kvp_status kvp_rank_begin(kvp_engine* e, const float* rows, int64_t n_rows, int6
         if (kv_bufs) R.ext_kv.assign(kv_bufs, kv_bufs + 2 * s.L);
         R.profiling = e->profiling;
         R.decode = false;
+        R.pos0 = start;
+        R.rope_inv = e->rope_table(0);
+        R.rope_hd = R.rope_inv ? static_cast<int>(s.hd) : 0;
         R.n_mirror = 0;
         R.mirror_bufs.clear();
         R.marks.clear();

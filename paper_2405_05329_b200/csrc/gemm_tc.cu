@@ -115,17 +115,44 @@ struct EpiArgs {
     bf16* mk[8];  // EPI_QKV mirrors of the K / V columns (GemmEpilogue::mirror_k/v)
     bf16* mv[8];
     int n_mirror;
+    int rope_hd;  // EPI_ROPE kinds: GemmEpilogue::rope_*
+    int64_t rope_pos0;
+    const float* rope_inv_freq;
 };
 
+// EPI_QKV / EPI_QKV_MIRROR | EPI_ROPE: the same epilogue with the rotary embedding applied to
+// the Q and K columns (a separate instantiation: the parity path carries none of it)
+constexpr int EPI_ROPE = 8;
+
+// Rotary embedding of one 32-column chunk of the Q or K region (region-relative first column
+// rc0, a multiple of 32; head_dim a multiple of 32, so a chunk never straddles a head): pair
+// (2i, 2i+1) of the head rotates by pos * inv_freq[i], f32 sincos with full range reduction.
+__device__ __forceinline__ void rope_chunk(float (&v)[32], int64_t rc0, int64_t pos, int hd,
+                                           const float* __restrict__ inv_freq) {
+    const int d0 = static_cast<int>(rc0 % hd);
+    const float fpos = static_cast<float>(pos);
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+        float sn, cs;
+        sincosf(fpos * __ldg(inv_freq + ((d0 + j) >> 1)), &sn, &cs);
+        const float x0 = v[j], x1 = v[j + 1];
+        v[j] = x0 * cs - x1 * sn;
+        v[j + 1] = x0 * sn + x1 * cs;
+    }
+}
+
 // QKV split / ReLU / plain bf16 store of one 32-column chunk (lane = row).
-template <int KIND>
+template <int KIND_>
 __device__ __forceinline__ void store_chunk(const EpiArgs& ep, int64_t row, int64_t col0, int64_t N,
                                             const uint32_t (&r)[32], float row_scale) {
+    constexpr int KIND = KIND_ & ~EPI_ROPE;
+    constexpr bool ROPE = (KIND_ & EPI_ROPE) != 0;
     const bool full = col0 + 32 <= N;
     {
         bf16* o;
         int region = 0;  // EPI_QKV: 1 = K, 2 = V chunk (also stored to the mirrors)
         int64_t region_off = 0;
+        int64_t rc0 = col0;  // region-relative first column (RoPE)
         if constexpr (KIND == EPI_QKV || KIND == EPI_QKV_MIRROR) {
             // chunks straddling the Q|K|V column boundaries (q or kv not a multiple of 32)
             // take the per-element path
@@ -153,6 +180,7 @@ __device__ __forceinline__ void store_chunk(const EpiArgs& ep, int64_t row, int6
                 o = ep.out1 + row * ep.ld1 + (col0 - ep.n0);
                 region_off = row * ep.ld1 + (col0 - ep.n0);
                 region = 1;
+                rc0 = col0 - ep.n0;
             } else {
                 o = ep.out2 + row * ep.ld2 + (col0 - ep.n0 - ep.n1);
                 region_off = row * ep.ld2 + (col0 - ep.n0 - ep.n1);
@@ -167,6 +195,8 @@ __device__ __forceinline__ void store_chunk(const EpiArgs& ep, int64_t row, int6
             v[j] = __uint_as_float(r[j]) * row_scale;
             if constexpr (KIND == EPI_RELU) v[j] = v[j] < 0.f ? 0.f : v[j];
         }
+        if constexpr (ROPE)
+            if (region != 2) rope_chunk(v, rc0, ep.rope_pos0 + row, ep.rope_hd, ep.rope_inv_freq);
         if (full) {
 #pragma unroll
             for (int j = 0; j < 32; j += 8) {
@@ -611,17 +641,23 @@ void dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
               const GemmEpilogue& g, cudaStream_t s) {
     EpiArgs ep{g.out0, g.ld0, g.n0, g.out1, g.ld1, g.n1, g.out2, g.ld2, g.outf, g.ldf, g.resid, g.ldr,
                g.outb, g.ldb, g.ssq_out, g.ssq_in, g.ssq_parts, g.norm_cols ? 1.0f / static_cast<float>(g.norm_cols) : 0.f,
-               {}, {}, g.kind == EPI_QKV ? g.n_mirror : 0};
+               {}, {}, g.kind == EPI_QKV ? g.n_mirror : 0, g.rope_hd, g.rope_pos0, g.rope_inv_freq};
     for (int m = 0; m < ep.n_mirror; ++m) {
         ep.mk[m] = g.mirror_k[m];
         ep.mv[m] = g.mirror_v[m];
     }
     switch (g.kind) {
         case EPI_QKV:
-            if (ep.n_mirror > 0)
+            if (ep.rope_hd > 0) {
+                if (ep.n_mirror > 0)
+                    launch_tc<BN, EPI_QKV_MIRROR | EPI_ROPE, NCTA>(ta, tb, tbh, M, N, K, ep, s);
+                else
+                    launch_tc<BN, EPI_QKV | EPI_ROPE, NCTA>(ta, tb, tbh, M, N, K, ep, s);
+            } else if (ep.n_mirror > 0) {
                 launch_tc<BN, EPI_QKV_MIRROR, NCTA>(ta, tb, tbh, M, N, K, ep, s);
-            else
+            } else {
                 launch_tc<BN, EPI_QKV, NCTA>(ta, tb, tbh, M, N, K, ep, s);
+            }
             break;
         case EPI_RESID: launch_tc<BN, EPI_RESID, NCTA>(ta, tb, tbh, M, N, K, ep, s); break;
         case EPI_RELU: launch_tc<BN, EPI_RELU, NCTA>(ta, tb, tbh, M, N, K, ep, s); break;

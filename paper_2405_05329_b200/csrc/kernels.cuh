@@ -85,6 +85,13 @@ struct GemmEpilogue {
     bf16* mirror_k[8] = {};
     bf16* mirror_v[8] = {};
     int n_mirror = 0;
+    // EPI_QKV only, opt-in extension (the reference model has no positional encoding): rotary
+    // embedding of the Q and K columns before they are stored (and mirrored).  Pairs
+    // (2i, 2i+1) of every head (head_dim rope_hd) of row r rotate by angle
+    // (rope_pos0 + r) * rope_inv_freq[i] (device table of rope_hd/2 floats).  rope_hd = 0: off.
+    int rope_hd = 0;
+    int64_t rope_pos0 = 0;
+    const float* rope_inv_freq = nullptr;
 };
 constexpr int KVP_MAX_MIRRORS = 8;
 inline int ssq_parts_for(int64_t cols) { return static_cast<int>((cols + 63) / 64); }

@@ -139,6 +139,7 @@ _SIGS = {
     "kvp_prefill_cached": (C.c_int, [_P, _P, _P, C.c_int64, _P, _P, C.POINTER(C.c_float)]),
     "kvp_decode": (C.c_int, [_P, _P, _P, C.c_int64, _P, C.POINTER(C.c_float)]),
     "kvp_forward_serial": (C.c_int, [_P, _P, C.c_int64, _P, _P]),
+    "kvp_engine_set_rope": (C.c_int, [_P, C.c_double]),
     "kvp_random_context": (C.c_int, [C.c_int64, C.c_int64, C.c_uint64, _P]),
     "kvp_random_context_device": (C.c_int, [_P, C.c_int64, C.c_uint64, _P]),
     "kvp_layer_qkv": (C.c_int, [_P, C.c_int64, _P, C.c_int64, _P, _P, _P]),
@@ -393,6 +394,13 @@ class WeightSet:
     def load_layer(self, layer: int, wq, wk, wv, wo, w1, w2) -> None:
         mats = [_f32(x) for x in (wq, wk, wv, wo, w1, w2)]
         _check(lib().kvp_engine_load_layer(self._h, layer, *[_vp(m) for m in mats]), "load_layer")
+
+    def set_rope(self, theta: float) -> None:
+        """Opt-in rotary position embedding (an extension: the reference model has none).
+        theta > 0 rotates pairs (2i, 2i+1) of every Q and K head at absolute position t by
+        t * theta^(-2i/head_dim) inside the QKV projection (bf16 engines, head_dim % 32 == 0);
+        theta <= 0 turns it off."""
+        _check(lib().kvp_engine_set_rope(self._h, float(theta)), "set_rope")
 
     def close(self) -> None:
         if getattr(self, "_h", None):
