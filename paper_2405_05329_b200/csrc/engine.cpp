@@ -1661,13 +1661,15 @@ kvp_status kvp_rank_end(kvp_engine* e, float* out_rows, int32_t out_on_device, f
         std::lock_guard<std::mutex> g(e->mu);
         RankCtx& R = session_rank(e);
         const Shape& s = e->s;
+        // the first-token row's D2H is inside the timed span (it is part of TTFT); the optional
+        // full hidden block copy is not
+        if (last_row)
+            KVP_CUDA(cudaMemcpyAsync(last_row, R.h.as<float>() + (e->sess_rows - 1) * s.d, s.d * 4,
+                                     cudaMemcpyDeviceToHost, R.comp));
         KVP_CUDA(cudaEventRecord(R.ev_done, R.comp));
         if (out_rows)
             KVP_CUDA(cudaMemcpyAsync(out_rows, R.h.p, e->sess_rows * s.d * 4,
                                      out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, R.comp));
-        if (last_row)
-            KVP_CUDA(cudaMemcpyAsync(last_row, R.h.as<float>() + (e->sess_rows - 1) * s.d, s.d * 4,
-                                     cudaMemcpyDeviceToHost, R.comp));
         KVP_CUDA(cudaStreamSynchronize(R.comp));
         float t = 0.f;
         KVP_CUDA(cudaEventElapsedTime(&t, R.ev_begin, R.ev_done));

@@ -15,10 +15,20 @@ slot to a CLOSED tombstone, DuplicateMessage re-queues the message so every late
 shifted.  Receivers validate headers exactly like recv_checked (engine.hpp:166-179) after the
 run; the first error (lowest layer, then rank) is agreed over the group and raised on every
 rank, like Fabric::abort_all + rethrow_if_failed (channel.hpp:120-136).
+
+Hang safety of the peer-memory transport: its flag waits are enqueued on the GPU
+(cuStreamWaitValue32), so a peer that dies or never signals would block the stream for good.
+Before reading its result each rank polls its streams against a deadline
+(KVP_PEER_TIMEOUT_S, default 120 s); on expiry it writes the awaited values into its OWN flag
+words from a side stream (the stuck waits release, the stream drains), drops the peer
+mappings, and reports a ProtocolError that the post-run agreement raises on every rank -- the
+analogue of Channel::close waking blocked receivers (channel.hpp:15-18, 120-136).
 """
 from __future__ import annotations
 
 import collections
+import os
+import time
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -309,6 +319,37 @@ def _wait(stream: int, flag: int, value: int):
     kv._check(kv.lib().kvp_stream_wait(C.c_void_p(stream), C.c_void_p(flag), value), "stream_wait")
 
 
+def _peer_timeout_s() -> float:
+    return float(os.environ.get("KVP_PEER_TIMEOUT_S", "120"))
+
+
+def _silent_rank() -> int:
+    """Hang-safety test hook: KVP_PEER_SILENT_RANK=r makes rank r skip every flag signal of
+    the peer transport (a peer that never delivers), so its receivers must time out."""
+    return int(os.environ.get("KVP_PEER_SILENT_RANK", "-1"))
+
+
+def _drain_or_release(executor, ps, top_value: int, timeout_s: float) -> bool:
+    """Waits until the rank's compute and comm streams are idle.  True if they drained in
+    time; otherwise releases the rank's own stuck flag waits (writes top_value, the largest
+    flag value of this run, into every flag slot from a side stream), lets the streams drain
+    and returns False (the caller agrees the error and every rank drops its peer session)."""
+    streams = (executor._stream, ps.comm)
+    deadline = time.monotonic() + timeout_s
+    while not all(s.query() for s in streams):
+        if time.monotonic() > deadline:
+            torch = executor.torch
+            side = torch.cuda.Stream(device=executor.device)
+            for slot in range(_FLAG_SLOTS):
+                _signal(side.cuda_stream, ps.my_flag(slot), top_value)
+            side.synchronize()
+            for s in streams:
+                s.synchronize()
+            return False
+        time.sleep(0.0005)
+    return True
+
+
 def _copy(stream: int, dst: int, src: int, nbytes: int):
     import ctypes as C
     kv._check(kv.lib().kvp_stream_copy(C.c_void_p(stream), C.c_void_p(dst), C.c_void_p(src), nbytes), "stream_copy")
@@ -415,6 +456,7 @@ def run_rank(strategy: kv.Strategy, rows, partition: kv.ContextPartition, execut
         targets = ([rank + 1] if rank + 1 < p else []) if strategy == kv.Strategy.KVR else \
             [j for j in range(p) if j != rank]
         executor.set_mirrors([ps.peers[j]["kv"] for j in targets])
+        signal = _signal if _silent_rank() != rank else (lambda *_: None)
     for layer in range(n_layers):
         executor.qkv(layer)
         K, V = executor.kv(layer)
@@ -423,7 +465,7 @@ def run_rank(strategy: kv.Strategy, rows, partition: kv.ContextPartition, execut
             if strategy == kv.Strategy.KVR:
                 OWN, PREFIX = 0, 1
                 if rank + 1 < p:
-                    _signal(comp, ps.flag(rank + 1, OWN), v)  # rows [start, stop) are at rank+1
+                    signal(comp, ps.flag(rank + 1, OWN), v)  # rows [start, stop) are at rank+1
                     sent_ctr[0] += stop
                 if rank > 0:
                     waits += 1
@@ -436,11 +478,11 @@ def run_rank(strategy: kv.Strategy, rows, partition: kv.ContextPartition, execut
                         dst = ps.peers[rank + 1]["kv"]
                         _copy(comm, dst[2 * layer], K.data_ptr(), start * row_bytes)
                         _copy(comm, dst[2 * layer + 1], V.data_ptr(), start * row_bytes)
-                        _signal(comm, ps.flag(rank + 1, PREFIX), v)
+                        signal(comm, ps.flag(rank + 1, PREFIX), v)
                 k_rows = stop
             else:
                 for j in targets:
-                    _signal(comp, ps.flag(j, rank), v)
+                    signal(comp, ps.flag(j, rank), v)
                 for j in targets:
                     _wait(comp, ps.my_flag(j), v)
                     sent_ctr[0] += stop - start
@@ -516,14 +558,17 @@ def run_rank(strategy: kv.Strategy, rows, partition: kv.ContextPartition, execut
                 w.wait()
         if use_peer:  # the prefix forwards are part of this rank's run
             executor._stream.wait_stream(ps.comm)
+    err = None
+    if use_peer and not _drain_or_release(executor, ps, (ps.epoch + 1) * n_layers, _peer_timeout_s()):
+        err = (-1, rank, _ERR_CODES[kv.ProtocolError],
+               f"peer handoff timed out after {_peer_timeout_s():g} s (a peer never signalled its K/V rows)")
     hidden, ms = executor.end()
     sent = sent_ctr[0]
 
     # deferred recv_checked: first error by (layer, rank), agreed over the group
-    err = None
     for hin, kind, layer, lo, hi in inbound:
         res = _check_header(hin.cpu().tolist() if hasattr(hin, "cpu") else hin, kind, layer, lo, hi)
-        if res is not None:
+        if res is not None and err is None:
             err = (layer, rank, _ERR_CODES[res[0]], res[1])
             break
     everyone = [None] * world
@@ -531,6 +576,10 @@ def run_rank(strategy: kv.Strategy, rows, partition: kv.ContextPartition, execut
                                       "last": hidden[-1:].tolist() if rank == world - 1 else None},
                            group=group)
     errs = [e["err"] for e in everyone if e["err"] is not None]
+    if errs and use_peer:
+        # collective teardown: every rank re-exchanges handles and restarts its flag epochs
+        # together on the next run
+        executor.close()
     if errs:
         first = min(errs, key=lambda t: (t[0], t[1]))
         raise _ERR_BY_CODE[first[2]](f"rank {first[1]}: {first[3]}")

@@ -195,3 +195,63 @@ def test_decode_on_last_rank_after_kvr():
     full = kv.run(kv.Strategy.Serial, O.random_context(335, 1024, 13, np.float32), kv.even_partition(335, 1), W)
     assert np.array_equal(got[0], got[1])
     assert np.array_equal(got[1], full.hidden_out[331:335])
+
+
+def _silent_worker(rank, world, port, strategy, outq):
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import oracle as O
+    from paper_2405_05329_b200 import kvprefill as kv
+    from paper_2405_05329_b200.distributed import GpuExecutor, Transport, run_rank
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    W = kv.init_weights(kv.ModelConfig(1024, 8, 2, 2, 5, "bf16", True), [0])
+    ex = GpuExecutor(W, 0)
+    tr = Transport(peer=True)
+    strat = kv.Strategy.KVR if strategy == "kvr" else kv.Strategy.TSP
+    b = [0, 300, 517] if world == 2 else [0, 200, 390, 517]
+    ctx = O.random_context(517, 1024, 11, np.float32)
+    part = kv.ContextPartition(517, b)
+    os.environ["KVP_PEER_SILENT_RANK"] = "0"
+    os.environ["KVP_PEER_TIMEOUT_S"] = "3"
+    err = None
+    try:
+        run_rank(strat, ctx[b[rank]:b[rank + 1]], part, ex, tr, rank, world, 2)
+    except kv.ProtocolError as e:
+        err = str(e)
+    # the streams drained and the mappings were dropped: the next run on the same executors works
+    os.environ["KVP_PEER_SILENT_RANK"] = "-1"
+    res = run_rank(strat, ctx[b[rank]:b[rank + 1]], part, ex, tr, rank, world, 2)
+    outq.put((rank, (err, res.hidden_rows)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("strategy,world", [("kvr", 2), ("kvr", 3), ("tsp", 2)])
+def test_peer_handoff_dead_peer_raises_protocol_error(strategy, world):
+    """Hang safety of the peer-memory transport: rank 0 never signals (KVP_PEER_SILENT_RANK),
+    so its receivers' GPU-side flag waits would block forever; the watchdog releases them after
+    KVP_PEER_TIMEOUT_S and EVERY rank raises ProtocolError (the reference's abort_all wakes all
+    blocked receivers, channel.hpp:120-136).  The same executors then run cleanly, bitwise
+    equal to the serial run."""
+    from paper_2405_05329_b200 import kvprefill as kv
+    if kv.device_count() == 0:
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_silent_worker, args=(r, world, port, strategy, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert got[r][0] is not None and "timed out" in got[r][0], got[r][0]
+    import oracle as O
+    W = kv.init_weights(kv.ModelConfig(1024, 8, 2, 2, 5, "bf16", True), [0])
+    ref = kv.run(kv.Strategy.Serial, O.random_context(517, 1024, 11, np.float32), kv.even_partition(517, 1), W)
+    assert np.array_equal(np.concatenate([got[r][1] for r in range(world)]), ref.hidden_out)
