@@ -21,10 +21,12 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 #include <stdexcept>
 
 #include "kernels.cuh"
 #include "ptx.cuh"
+#include "softmax.cuh"
 
 namespace kvp {
 
@@ -32,6 +34,7 @@ bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t 
                     uint32_t box_inner, uint32_t box_outer);
 
 namespace {
+using namespace smx;
 
 constexpr int BQ = 128;  // queries per tile (NT tiles per CTA)
 // warp 0 TMA, warp 1 MMA, warps 2 .. 2+4*NT-1 softmax (four per query tile)
@@ -63,51 +66,6 @@ struct ACfg {
     static_assert(NEED + 512 <= 232448, "attention smem over the 227 KB opt-in limit");
 };
 
-// ---- packed f32x2 arithmetic (sm_100: FFMA2 / FADD2) and exp2 on two pipes ----
-__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
-    float2 d;
-    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
-        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
-        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
-        : "=f"(d.x), "=f"(d.y)
-        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-    return d;
-}
-__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
-    float2 d;
-    asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
-        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
-        "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
-        : "=f"(d.x), "=f"(d.y)
-        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-    return d;
-}
-// MUFU.EX2 (ex2(-inf) = +0 exactly)
-__device__ __forceinline__ float ex2_mufu(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-// 2^x on the FMA pipe: x = n + f with n = rint(x) (magic-number add), 2^f by a degree-3
-// minimax polynomial on [-1/2, 1/2] (max rel. error 1.0e-4, far below bf16's 3.9e-3), 2^n
-// added into the exponent bits.  x is clamped at -125 (masked lanes are zeroed by the
-// caller), x <= 8 by the rescale threshold.
-__device__ __forceinline__ float2 ex2_poly2(float2 x) {
-    x.x = fmaxf(x.x, -125.f);
-    x.y = fmaxf(x.y, -125.f);
-    const float2 magic = make_float2(12582912.f, 12582912.f), neg1 = make_float2(-1.f, -1.f);
-    const float2 t = fadd2(x, magic);
-    const float2 n = fadd2(t, make_float2(-12582912.f, -12582912.f));
-    const float2 f = ffma2(n, neg1, x);
-    float2 p = ffma2(make_float2(0.055008821f, 0.055008821f), f, make_float2(0.24221078f, 0.24221078f));
-    p = ffma2(p, f, make_float2(0.6932829f, 0.6932829f));
-    p = ffma2(p, f, make_float2(1.f, 1.f));
-    float2 r;
-    r.x = __uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23));
-    r.y = __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23));
-    return r;
-}
-
 struct AttnArgs {
     int64_t q_rows, k_rows, offset;
     int n_heads, group;
@@ -117,7 +75,14 @@ struct AttnArgs {
     int mma_wait;  // 1: the MMA issuer waits for PV(j) before S(j+1) reuses its TMEM columns
     uint32_t* trace;  // tuning only (KVP_ATTN_TRACE): SM clock of pipeline events of one CTA
     int trace_blk;
+    unsigned long long* cta_trace;  // tuning only (KVP_ATTN_CTA_TRACE): per CTA {start, end, smid, steps}
 };
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 // trace[ev * 512 + j] = clock() of event ev for key tile j, CTA (blockIdx.y * gridDim.x + blockIdx.x) == trace_blk
 #define ATTN_TRACE(ev, j)                                                                              \
@@ -152,6 +117,7 @@ __global__ void __launch_bounds__(threads_for<NT>(), 1)
     uint64_t* o_done = p_full + NT;          // [NT] query tiles
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + NT);
 
+    const unsigned long long t_start = a.cta_trace && threadIdx.x == 0 ? globaltimer() : 0;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int num_groups = static_cast<int>((a.q_rows + NT * BQ - 1) / (NT * BQ));
     // grid = (heads, query groups): the block scheduler walks x fastest, so ALL heads of the
@@ -226,57 +192,60 @@ __global__ void __launch_bounds__(threads_for<NT>(), 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc_s = ptx::idesc_bf16(BQ, BKV, 0);
-            constexpr uint32_t idesc_o = ptx::idesc_bf16(BQ, HD, 1);  // B = V is MN-major
-            auto issue_s = [&](int x, int t) {
-                const int s = t % KST;
-                ptx::mbar_wait(&k_full[s], (t / KST) & 1);
-                ptx::tc_fence_after();
-                if (x < 2) ATTN_TRACE(0 + x, t);
-                const uint32_t q_addr = ptx::smem_u32(sQ + x * C::Q_BYTES);
-                const uint32_t k_addr = ptx::smem_u32(sK + s * C::KV_BYTES);
+        // the whole warp runs the issue loop converged; one elected lane issues each
+        // tcgen05.mma / commit (ptx::*_w).  Descriptors are built once and advanced by
+        // constant offsets (the 14-bit address field holds addr >> 4).
+        constexpr uint32_t idesc_s = ptx::idesc_bf16(BQ, BKV, 0);
+        constexpr uint32_t idesc_o = ptx::idesc_bf16(BQ, HD, 1);  // B = V is MN-major
+        const uint64_t qdesc0 = ptx::smem_desc_sw128(ptx::smem_u32(sQ), 16, 1024);
+        const uint64_t kdesc0 = ptx::smem_desc_sw128(ptx::smem_u32(sK), 16, 1024);
+        const uint64_t vdesc0 = ptx::smem_desc_sw128(ptx::smem_u32(sV), BKV * 128, 1024);
+        auto issue_s = [&](int x, int t) {
+            const int s = t % KST;
+            ptx::mbar_wait(&k_full[s], (t / KST) & 1);
+            ptx::tc_fence_after();
+            if (x < 2 && lane == 0) ATTN_TRACE(0 + x, t);
+            const uint64_t qd = qdesc0 + static_cast<uint64_t>((x * C::Q_BYTES) >> 4);
+            const uint64_t kd = kdesc0 + static_cast<uint64_t>((s * C::KV_BYTES) >> 4);
 #pragma unroll
-                for (int k = 0; k < HD / 16; ++k) {
-                    const uint32_t off = (k >> 2) * (BQ * 128) + (k & 3) * 32;
-                    const uint64_t ad = ptx::smem_desc_sw128(q_addr + off, 16, 1024);
-                    const uint64_t bd = ptx::smem_desc_sw128(k_addr + (k >> 2) * (BKV * 128) + (k & 3) * 32, 16, 1024);
-                    ptx::mma_bf16_ss(tmem + x * BKV, ad, bd, idesc_s, k != 0);
-                }
-                ptx::mma_commit(&s_full[x]);
-                if (x == NT - 1) ptx::mma_commit(&k_empty[s]);  // the last tile is the last reader of K(t)
-            };
-            auto issue_pv = [&](int x, int t) {
-                const int s = t % VST;
-                ptx::mbar_wait(&p_full[x], t & 1);
-                ptx::mbar_wait(&v_full[s], (t / VST) & 1);
-                ptx::tc_fence_after();
-                if (x < 2) ATTN_TRACE(2 + x, t);
-                const uint32_t v_addr = ptx::smem_u32(sV + s * C::KV_BYTES);
+            for (int k = 0; k < HD / 16; ++k) {
+                const uint64_t off_q = ((k >> 2) * (BQ * 128) + (k & 3) * 32) >> 4;
+                const uint64_t off_k = ((k >> 2) * (BKV * 128) + (k & 3) * 32) >> 4;
+                ptx::mma_bf16_ss_w(tmem + x * BKV, qd + off_q, kd + off_k, idesc_s, k != 0);
+            }
+            ptx::mma_commit_w(&s_full[x]);
+            if (x == NT - 1) ptx::mma_commit_w(&k_empty[s]);  // the last tile is the last reader of K(t)
+        };
+        auto issue_pv = [&](int x, int t) {
+            const int s = t % VST;
+            ptx::mbar_wait(&p_full[x], t & 1);
+            ptx::mbar_wait(&v_full[s], (t / VST) & 1);
+            ptx::tc_fence_after();
+            if (x < 2 && lane == 0) ATTN_TRACE(2 + x, t);
+            const uint64_t vd = vdesc0 + static_cast<uint64_t>((s * C::KV_BYTES) >> 4);
 #pragma unroll
-                for (int k = 0; k < BKV / 16; ++k) {
-                    // B = V[keys 16k..16k+15][hd]: MN-major SW128, LBO = next 64-wide hd block,
-                    // SBO = next 8 keys.
-                    const uint64_t bd = ptx::smem_desc_sw128(v_addr + k * 16 * 128, BKV * 128, 1024);
-                    ptx::mma_bf16_ts(tmem + C::O_BASE + x * HD, tmem + x * BKV + k * 8, bd, idesc_o, (t | k) != 0);
-                }
-                ptx::mma_commit(&o_done[x]);
-                if (x == NT - 1) ptx::mma_commit(&v_empty[s]);  // the last tile is the last reader of V(t)
-            };
-            ptx::mbar_wait(q_full, 0);
-            for (int x = 0; x < NT; ++x) issue_s(x, 0);
-            for (int j = 0; j < n_kt[NT - 1]; ++j) {
+            for (int k = 0; k < BKV / 16; ++k) {
+                // B = V[keys 16k..16k+15][hd]: MN-major SW128, LBO = next 64-wide hd block,
+                // SBO = next 8 keys.
+                ptx::mma_bf16_ts_w(tmem + C::O_BASE + x * HD, tmem + x * BKV + k * 8,
+                                   vd + static_cast<uint64_t>((k * 16 * 128) >> 4), idesc_o, (t | k) != 0);
+            }
+            ptx::mma_commit_w(&o_done[x]);
+            if (x == NT - 1) ptx::mma_commit_w(&v_empty[s]);  // the last tile is the last reader of V(t)
+        };
+        ptx::mbar_wait(q_full, 0);
+        for (int x = 0; x < NT; ++x) issue_s(x, 0);
+        for (int j = 0; j < n_kt[NT - 1]; ++j) {
 #pragma unroll
-                for (int x = 0; x < NT; ++x) {
-                    if (j >= n_kt[x]) continue;
-                    issue_pv(x, j);
-                    if (j + 1 < n_kt[x]) {
-                        // S_x(j+1) overwrites the TMEM columns P_x(j) is read from: tcgen05.mma
-                        // ops of one thread execute in issue order, so waiting for PV_x(j) is
-                        // only needed when the pipeline is not trusted (a.mma_wait)
-                        if (a.mma_wait) ptx::mbar_wait(&o_done[x], j & 1);
-                        issue_s(x, j + 1);
-                    }
+            for (int x = 0; x < NT; ++x) {
+                if (j >= n_kt[x]) continue;
+                issue_pv(x, j);
+                if (j + 1 < n_kt[x]) {
+                    // S_x(j+1) overwrites the TMEM columns P_x(j) is read from: tcgen05.mma
+                    // ops of one thread execute in issue order, so waiting for PV_x(j) is
+                    // only needed when the pipeline is not trusted (a.mma_wait)
+                    if (a.mma_wait) ptx::mbar_wait(&o_done[x], j & 1);
+                    issue_s(x, j + 1);
                 }
             }
         }
@@ -292,11 +261,14 @@ __global__ void __launch_bounds__(threads_for<NT>(), 1)
         const uint32_t lane_base = tmem + ((quarter * 32u) << 16);
         const int nt = n_kt[x];
         const float2 sl2v = make_float2(a.sl2, a.sl2);
+        const float2 sl2y = make_float2(a.sl2 * (1.f / 256.f), a.sl2 * (1.f / 256.f));
         float m_run = -INFINITY, l = 0.f;
         // exp2 of the row's BKV scores against base m (log2 units), P -> TMEM as packed bf16
         // over the first BKV/2 S columns; returns the row sum of P
         auto exp_store = [&](const float (&sv)[BKV], float m, bool diag) -> float {
             const float2 nb2 = make_float2(-m, -m);
+            // poly columns: y = sat(x / 256 + POLY_BIAS / 256) straight from the score
+            const float2 yb2 = make_float2((POLY_BIAS - m) * (1.f / 256.f), (POLY_BIAS - m) * (1.f / 256.f));
             float2 lacc = make_float2(0.f, 0.f);
 #pragma unroll
             for (int c = 0; c < BKV / 32; ++c) {
@@ -304,16 +276,16 @@ __global__ void __launch_bounds__(threads_for<NT>(), 1)
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const int col = c * 32 + 2 * i;
-                    const float2 xv = ffma2(make_float2(sv[col], sv[col + 1]), sl2v, nb2);
                     float2 pv;
                     // NPOLY of every 16 column pairs take exp2 on the FMA pipe, the rest on MUFU
                     if (i >= 16 - NPOLY) {
-                        pv = ex2_poly2(xv);
+                        pv = ex2_poly_sat(ffma2_sat(make_float2(sv[col], sv[col + 1]), sl2y, yb2));
                         if (diag) {  // the FMA-pipe exp2 clamps -inf: zero masked keys
                             pv.x = sv[col] == -INFINITY ? 0.f : pv.x;
                             pv.y = sv[col + 1] == -INFINITY ? 0.f : pv.y;
                         }
                     } else {
+                        const float2 xv = ffma2(make_float2(sv[col], sv[col + 1]), sl2v, nb2);
                         pv.x = ex2_mufu(xv.x);
                         pv.y = ex2_mufu(xv.y);
                     }
@@ -350,15 +322,16 @@ __global__ void __launch_bounds__(threads_for<NT>(), 1)
 #pragma unroll
                 for (int i = 0; i < BKV; ++i) sv[i] = i < nvis ? sv[i] : -INFINITY;
             }
-            float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+            // row max: four independent FMNMX3 chains (two new columns per instruction)
+            static_assert(BKV % 8 == 0, "row max layout");
+            float m4[4] = {sv[0], sv[1], sv[2], sv[3]};
 #pragma unroll
-            for (int i = 0; i < BKV; i += 8) {
-                m4[0] = fmaxf(m4[0], fmaxf(sv[i + 0], sv[i + 4]));
-                m4[1] = fmaxf(m4[1], fmaxf(sv[i + 1], sv[i + 5]));
-                m4[2] = fmaxf(m4[2], fmaxf(sv[i + 2], sv[i + 6]));
-                m4[3] = fmaxf(m4[3], fmaxf(sv[i + 3], sv[i + 7]));
+            for (int i = 4; i + 8 <= BKV; i += 8) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) m4[k] = fmax3(m4[k], sv[i + k], sv[i + 4 + k]);
             }
-            const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * a.sl2;  // scale > 0
+            const float mx = fmax3(fmax3(m4[0], m4[1], sv[BKV - 4]), fmax3(m4[2], m4[3], sv[BKV - 3]),
+                                   fmaxf(sv[BKV - 2], sv[BKV - 1])) * a.sl2;  // scale > 0
             if (tr) ATTN_TRACE(8 + x, j);
             const bool need = mx > m_run + RESCALE_THRESHOLD;
             if (__any_sync(0xffffffffu, need)) {
@@ -418,6 +391,15 @@ __global__ void __launch_bounds__(threads_for<NT>(), 1)
         ptx::tc_fence_after();
         ptx::tmem_dealloc<TMEM_COLS>(tmem);
     }
+    if (a.cta_trace && threadIdx.x == 0) {
+        unsigned long long* r = a.cta_trace + 4 * (blockIdx.y * gridDim.x + blockIdx.x);
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        r[0] = t_start;
+        r[1] = globaltimer();
+        r[2] = smid;
+        r[3] = static_cast<unsigned long long>(n_kt[NT - 1]);
+    }
 }
 
 int mma_wait_flag() {
@@ -444,7 +426,21 @@ void launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShap
         configured = dev;
     }
     AttnArgs a{sh.q_rows, sh.k_rows, sh.offset, sh.n_heads, sh.n_heads / sh.n_kv_heads, sh.ldo, O,
-               (1.0f / sqrtf(static_cast<float>(HD))) * 1.4426950408889634f, mma_wait_flag(), nullptr, -1};
+               (1.0f / sqrtf(static_cast<float>(HD))) * 1.4426950408889634f, mma_wait_flag(), nullptr, -1, nullptr};
+    dim3 grid(static_cast<unsigned>(sh.n_heads), static_cast<unsigned>((sh.q_rows + NT * BQ - 1) / (NT * BQ)));
+    // tuning only: KVP_ATTN_CTA_TRACE=<file> records {start ns, end ns, smid, key steps} per CTA
+    static const char* cta_env = getenv("KVP_ATTN_CTA_TRACE");
+    const size_t n_cta = static_cast<size_t>(grid.x) * grid.y;
+    if (cta_env) {
+        static unsigned long long* cbuf = nullptr;
+        static size_t cap = 0;
+        if (cap < n_cta) {
+            if (cbuf) cudaFree(cbuf);
+            cudaMalloc(&cbuf, n_cta * 4 * sizeof(unsigned long long));
+            cap = n_cta;
+        }
+        a.cta_trace = cbuf;
+    }
     // tuning only: KVP_ATTN_TRACE=<cta> records one CTA's pipeline events into KVP_ATTN_TRACE_OUT
     static const char* trace_env = getenv("KVP_ATTN_TRACE");
     if (trace_env) {
@@ -454,7 +450,6 @@ void launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShap
         a.trace = buf;
         a.trace_blk = atoi(trace_env);
     }
-    dim3 grid(static_cast<unsigned>(sh.n_heads), static_cast<unsigned>((sh.q_rows + NT * BQ - 1) / (NT * BQ)));
     note_launch();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
@@ -467,6 +462,15 @@ void launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShap
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
     cudaLaunchKernelEx(&cfg, attn_tc_kernel<HD, NT, BKV, NPOLY>, tq, tk, tv, a);
+    if (a.cta_trace) {
+        std::vector<unsigned long long> host(n_cta * 4);
+        cudaMemcpyAsync(host.data(), a.cta_trace, host.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        if (FILE* f = fopen(cta_env, "wb")) {
+            fwrite(host.data(), host.size() * sizeof(unsigned long long), 1, f);
+            fclose(f);
+        }
+    }
     if (a.trace) {
         uint32_t host[16 * 512];
         cudaMemcpyAsync(host, a.trace, sizeof(host), cudaMemcpyDeviceToHost, s);
@@ -510,6 +514,16 @@ void attn_bf16_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const At
         return e ? atoi(e) : 2;
     }();
     const bool h128 = sh.head_dim == 128;
+    // hd 128: the double-buffered one-tile-per-CTA kernel (attn_tb.cu) on grids of up to four
+    // waves of 256-row CTAs -- the rank chunks of KV-Runahead (Llama 4k p=8 last rank: 767 vs
+    // 409 TF/s; 4k p=1: 920 vs 900), this kernel's two-tile CTAs on bigger grids (16k p=1:
+    // 1148 vs 1074 TF/s).  KVP_ATTN_TB=0 / 1 forces either.
+    static const int tb = [] {
+        const char* e = getenv("KVP_ATTN_TB");
+        return e ? atoi(e) : -1;
+    }();
+    const int64_t ctas256 = static_cast<int64_t>(sh.n_heads) * ((sh.q_rows + 255) / 256);
+    if (h128 && (tb == 1 || (tb < 0 && ctas256 <= 4 * 148))) return attn_bf16_tb(Q, K, V, O, sh, s);
     const int np = poly >= 0 ? poly : (h128 ? DEFAULT_POLY_128 : DEFAULT_POLY_64);
     if (h128)
         launch_poly<128, 2, 128>(np, Q, K, V, O, sh, s);

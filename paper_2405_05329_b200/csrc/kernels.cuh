@@ -122,6 +122,8 @@ void attn_bf16(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnS
 // the two implementations behind attn_bf16: tcgen05/TMEM (default) and warp-level mma.sync
 bool attn_tc_supported(int head_dim);
 void attn_bf16_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShape& sh, cudaStream_t s);
+// head_dim 128, one query tile per CTA, S triple-buffered in TMEM (attn_tb.cu)
+void attn_bf16_tb(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShape& sh, cudaStream_t s);
 void attn_bf16_mma(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShape& sh, cudaStream_t s);
 // Generic SIMT attention (any head_dim <= 256): f32 math; T = float or bf16 I/O.
 void attn_simt_f32(const float* Q, const float* K, const float* V, float* O, const AttnShape& sh,

@@ -23,7 +23,8 @@ from typing import Callable, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libkvp_b200.so")
+# KVP_LIB_PATH: A/B tuning only (an alternative build of the same library)
+LIB_PATH = os.environ.get("KVP_LIB_PATH") or os.path.join(_HERE, "_lib", "libkvp_b200.so")
 MAX_RANKS = 64
 
 

@@ -4,7 +4,11 @@ per process) against the oracle and the default path: each variant runs in a sub
                           in-order execution; results must be bitwise identical)
   KVP_ATTN_HD64_TILES=3   head_dim 64 with three query tiles x 96-key tiles
   KVP_ATTN_POLY=2         part of the exp2 on the FMA pipe (degree-3 polynomial)
-  KVP_PDL=0               no programmatic dependent launch (bitwise identical)"""
+  KVP_PDL=0               no programmatic dependent launch (bitwise identical)
+  KVP_ATTN_TB=0 / 1       head_dim 128 forced onto the two-tile CTAs (attn_tc.cu) / the
+                          one-tile double-buffered kernel (attn_tb.cu); the default picks by
+                          grid size.  Row sums are added in a different order in the two
+                          kernels, so they agree to bf16 rounding, not bitwise"""
 import json
 import os
 import subprocess
@@ -57,11 +61,13 @@ def default():
 
 
 @pytest.mark.parametrize("env,bitwise", [({"KVP_ATTN_MMA_WAIT": "1"}, True), ({"KVP_PDL": "0"}, True),
-                                         ({"KVP_ATTN_HD64_TILES": "3"}, False), ({"KVP_ATTN_POLY": "2"}, False)])
+                                         ({"KVP_ATTN_HD64_TILES": "3"}, False), ({"KVP_ATTN_POLY": "2"}, False),
+                                         ({"KVP_ATTN_TB": "0"}, False), ({"KVP_ATTN_TB": "1"}, False),
+                                         ({"KVP_ATTN_TB": "1", "KVP_ATTN_POLY": "4"}, False)])
 def test_attention_variant(default, env, bitwise):
     got = _run(env)
     for d, res in got.items():
         assert res["dev"] <= 3e-2, (env, d, res)          # bf16 attention vs the f64 oracle
         assert res["split_equal"], (env, d)              # split invariance holds in every variant
-        if bitwise or (env.get("KVP_ATTN_HD64_TILES") and d == "1024"):
+        if bitwise or (env.get("KVP_ATTN_HD64_TILES") and d == "1024") or (env.get("KVP_ATTN_TB") and "KVP_ATTN_POLY" not in env and d == "512"):
             assert res["hash"] == default[d]["hash"], (env, d)
