@@ -350,6 +350,25 @@ def _drain_or_release(executor, ps, top_value: int, timeout_s: float) -> bool:
     return True
 
 
+def _warm_kernels(executor, rows, start: int, held: int, k_rows: int, n_layers: int):
+    """Runs this chunk shape once through the local layer executor (no peer, no flags, result
+    discarded) the first time it is seen.  CUDA loads kernels lazily at their first launch and
+    the load waits for the device to drain; in a peer run the first launches after a flag wait
+    (attention, FFN) would otherwise wait on a stream that is itself blocked on a peer -- a
+    dead peer would then hang the host before the watchdog can act."""
+    key = (id(executor.w), len(rows), start, held, k_rows)
+    seen = executor.__dict__.setdefault("_warm", set())
+    if key in seen:
+        return
+    executor.begin(rows, start, held)
+    executor.set_mirrors([])
+    for layer in range(n_layers):
+        executor.qkv(layer)
+        executor.finish(layer, k_rows)
+    executor.end()
+    seen.add(key)
+
+
 def _copy(stream: int, dst: int, src: int, nbytes: int):
     import ctypes as C
     kv._check(kv.lib().kvp_stream_copy(C.c_void_p(stream), C.c_void_p(dst), C.c_void_p(src), nbytes), "stream_copy")
@@ -425,6 +444,15 @@ def run_rank(strategy: kv.Strategy, rows, partition: kv.ContextPartition, execut
     start, stop = b[rank], b[rank + 1]
     c = stop - start
     held = stop if strategy == kv.Strategy.KVR else C_
+    no_fault = fault is None or fault.kind == kv.FaultInjection.Kind.None_
+    # fused peer-memory handoff (no fault injected: faults are message edits, so they keep
+    # the message path): the QKV epilogue stores this rank's K/V rows into the receivers'
+    # caches; KVR forwards the upstream prefix with one copy-engine copy per tensor as soon
+    # as it has landed; stream-ordered flags replace the messages
+    use_peer = (no_fault and p > 1 and strategy in (kv.Strategy.KVR, kv.Strategy.TSP) and transport.peer_ok(executor)
+            and (strategy == kv.Strategy.KVR or p - 1 <= 8))
+    if use_peer:
+        _warm_kernels(executor, rows, start, held, stop if strategy == kv.Strategy.KVR else C_, n_layers)
     executor.begin(rows, start, held)
 
     dots = sent = recvd = waits = 0
@@ -433,16 +461,9 @@ def run_rank(strategy: kv.Strategy, rows, partition: kv.ContextPartition, execut
     out_links = collections.defaultdict(_Link)
     sent_ctr = [0]
     in_flight = []  # KVR handoff sends still on the wire (joined before the rank's result)
-    no_fault = fault is None or fault.kind == kv.FaultInjection.Kind.None_
     sizes = [b[i + 1] - b[i] for i in range(p)]
     gather_collective = (strategy == kv.Strategy.TSP and no_fault and p > 1 and len(set(sizes)) == 1
                          and transport.collective_ok(executor))
-    # fused peer-memory handoff (no fault injected: faults are message edits, so they keep
-    # the message path): the QKV epilogue stores this rank's K/V rows into the receivers'
-    # caches; KVR forwards the upstream prefix with one copy-engine copy per tensor as soon
-    # as it has landed; stream-ordered flags replace the messages
-    use_peer = (no_fault and p > 1 and strategy in (kv.Strategy.KVR, kv.Strategy.TSP) and transport.peer_ok(executor)
-            and (strategy == kv.Strategy.KVR or p - 1 <= 8))
     if use_peer:
         if executor.peer is None:
             executor.peer = _PeerSession(executor)
