@@ -298,6 +298,9 @@ __global__ void __launch_bounds__(threads_for<NT>(), 1)
         };
         for (int j = 0; j < nt; ++j) {
             ptx::mbar_wait(&s_full[x], j & 1);
+            // PV_x(j-1) completed before S_x(j) (issued behind it): observe its phase every step,
+            // so no o_done phase completes unwaited (compute-sanitizer synccheck) -- free here
+            if (j > 0) ptx::mbar_wait(&o_done[x], (j - 1) & 1);
             ptx::tc_fence_after();
             const bool tr = quarter == 0 && lane == 0 && x < 2;
             if (tr) ATTN_TRACE(4 + x, j);
@@ -337,9 +340,7 @@ __global__ void __launch_bounds__(threads_for<NT>(), 1)
             if (__any_sync(0xffffffffu, need)) {
                 const float m_new = need ? mx : m_run;
                 const float alpha = need ? exp2f(m_run - m_new) : 1.0f;
-                if (j > 0) {
-                    ptx::mbar_wait(&o_done[x], (j - 1) & 1);
-                    ptx::tc_fence_after();
+                if (j > 0) {  // PV_x(j-1) complete: waited for at the top of the step
 #pragma unroll
                     for (int c = 0; c < HD / 16; ++c) {
                         uint32_t r[16];
