@@ -101,9 +101,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* p_full = s_free + NS;    // [NS] P_j in TMEM (4 warps of set j & 1)
     uint64_t* o_done = p_full + NS;    // [2] PV_j completion, alternating
     uint64_t* o_final = o_done + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 1);
+    uint64_t* l_ready = o_final + 1;  // [2 sets][4 lane quarters] row sum after the set's tile
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(l_ready + 8);
     float* xm = reinterpret_cast<float*>(smem + Q_BYTES + (KST + VST) * KV_BYTES + BAR_BYTES);  // [BQ] running max
-    float* xl = xm + BQ;                                                                      // [2][BQ] l, [2][BQ] m
+    float* xl = xm + BQ;                                                                      // [2][BQ] row sum by tile parity
 
     const unsigned long long t_start = a.cta_trace && threadIdx.x == 0 ? gtimer() : 0;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -137,6 +138,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         ptx::mbar_init(&o_done[0], 1);
         ptx::mbar_init(&o_done[1], 1);
         ptx::mbar_init(o_final, 1);
+        for (int s = 0; s < 8; ++s) ptx::mbar_init(&l_ready[s], 1);
         ptx::fence_barrier_init();
     }
     if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
@@ -241,7 +243,25 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t bar_in = (set == 0 ? 5u : 1u) + quarter, bar_out = (set == 0 ? 1u : 5u) + quarter;
         const float2 sl2v = make_float2(a.sl2, a.sl2);
         const float2 sl2y = make_float2(a.sl2 * (1.f / 256.f), a.sl2 * (1.f / 256.f));
-        float l = 0.f, m_l = -INFINITY;  // this set's row sum and the base it is relative to
+        // The row sum runs through the tiles in order, l_j = l_{j-1} * alpha_j + lsum_j -- the
+        // very operations and order of attn_tc.cu, so the two kernels give bitwise equal rows
+        // and Serial == KVR stays bitwise whichever kernel a rank's grid selects.  l_{j-1} comes
+        // from the other set; each set finalises its tile j one tile later (at j + 2, after the
+        // row-max handoff), when the other set has long published l_{j-1}.
+        float pend_alpha = 1.f, pend_lsum = 0.f;
+        int pend_j = -1;
+        auto finalize_l = [&]() {
+            float l_prev = 0.f;
+            if (pend_j > 0) {
+                ptx::mbar_wait(&l_ready[(1 - set) * 4 + quarter], ((pend_j - 1) >> 1) & 1);
+                l_prev = xl[((pend_j - 1) & 1) * BQ + xrow];
+            }
+            xl[(pend_j & 1) * BQ + xrow] = l_prev * pend_alpha + pend_lsum;
+            __threadfence_block();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&l_ready[set * 4 + quarter]);
+            pend_j = -1;
+        };
         for (int j = set; j < n; j += 2) {
             const int b = set;  // == j & 1
             ptx::mbar_wait(&s_full[b], (j >> 1) & 1);
@@ -307,10 +327,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 ptx::tmem_st_wait();
             }
-            if (m_new != m_l) {
-                l *= exp2f(m_l - m_new);  // 0 while l is still empty (m_l = -inf)
-                m_l = m_new;
-            }
+            // the row sum's rescale factor, exactly as attn_tc.cu applies it (1 when the max holds)
+            const float alpha_l = need ? exp2f(m_prev - m_new) : 1.0f;
+            if (pend_j >= 0) finalize_l();  // this set's previous tile (j - 2)
             // P_b was last read by PV_{j-2}: complete long ago (checked, not assumed)
             if (j >= 2) {
                 ptx::mbar_wait(&o_done[b], ((j - 2) >> 1) & 1);
@@ -343,21 +362,20 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 ptx::tmem_st16(lane_base + P_COL + b * (BK / 2) + c * 16, pk);
             }
-            l += lacc.x + lacc.y;
+            const float lsum = lacc.x + lacc.y;
             ptx::tmem_st_wait();
             ptx::tc_fence_before();
             __syncwarp();
             if (tr) TB_TRACE(6 + set, j);
             if (lane == 0) ptx::mbar_arrive(&p_full[b]);
+            pend_alpha = alpha_l;  // l_j is finalised at this set's next tile (or after the loop)
+            pend_lsum = lsum;
+            pend_j = j;
         }
-        // epilogue: both sets' row sums re-based to the final max; each set stores half the row
-        xl[set * BQ + xrow] = l;
-        xl[(2 + set) * BQ + xrow] = m_l;
+        if (pend_j >= 0) finalize_l();
+        // epilogue: l_{n-1} from whichever set ran the last tile; each set stores half the row
         ptx::named_sync(9 + quarter, 64);
-        const float lo = xl[(1 - set) * BQ + xrow], mo = xl[(3 - set) * BQ + xrow];
-        const float mf = fmaxf(m_l, mo);
-        const float lt = (m_l == mf ? l : l * exp2f(m_l - mf)) + (mo == mf ? lo : lo * exp2f(mo - mf));
-        const float inv = 1.0f / lt;
+        const float inv = 1.0f / xl[((n - 1) & 1) * BQ + xrow];
         ptx::mbar_wait(o_final, 0);
         ptx::tc_fence_after();
         bf16* orow = a.O + row * a.ldo + static_cast<int64_t>(h) * HD + set * 64;

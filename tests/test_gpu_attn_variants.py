@@ -7,8 +7,10 @@ per process) against the oracle and the default path: each variant runs in a sub
   KVP_PDL=0               no programmatic dependent launch (bitwise identical)
   KVP_ATTN_TB=0 / 1       head_dim 128 forced onto the two-tile CTAs (attn_tc.cu) / the
                           one-tile double-buffered kernel (attn_tb.cu); the default picks by
-                          grid size.  Row sums are added in a different order in the two
-                          kernels, so they agree to bf16 rounding, not bitwise"""
+                          grid size.  Both run the same per-row operations in the same order
+                          (the row sum is handed between attn_tb's softmax sets in tile order),
+                          so they are bitwise identical and Serial == KVR holds whichever
+                          kernel a rank's grid selects"""
 import json
 import os
 import subprocess
@@ -69,5 +71,5 @@ def test_attention_variant(default, env, bitwise):
     for d, res in got.items():
         assert res["dev"] <= 3e-2, (env, d, res)          # bf16 attention vs the f64 oracle
         assert res["split_equal"], (env, d)              # split invariance holds in every variant
-        if bitwise or (env.get("KVP_ATTN_HD64_TILES") and d == "1024") or (env.get("KVP_ATTN_TB") and "KVP_ATTN_POLY" not in env and d == "512"):
+        if bitwise or (env.get("KVP_ATTN_HD64_TILES") and d == "1024") or (env.get("KVP_ATTN_TB") and "KVP_ATTN_POLY" not in env):
             assert res["hash"] == default[d]["hash"], (env, d)
