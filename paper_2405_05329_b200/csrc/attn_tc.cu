@@ -516,9 +516,10 @@ void attn_bf16_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const At
     }();
     const bool h128 = sh.head_dim == 128;
     // hd 128: the double-buffered one-tile-per-CTA kernel (attn_tb.cu) on grids of up to four
-    // waves of 256-row CTAs -- the rank chunks of KV-Runahead (Llama 4k p=8 last rank: 767 vs
-    // 409 TF/s; 4k p=1: 920 vs 900), this kernel's two-tile CTAs on bigger grids (16k p=1:
-    // 1148 vs 1074 TF/s).  KVP_ATTN_TB=0 / 1 forces either.
+    // waves of 256-row CTAs -- the rank chunks of KV-Runahead (Llama 4k p=8 last rank: ~650 vs
+    // ~390 TF/s; 4k p=1: ~880 vs ~875), this kernel's two-tile CTAs on bigger grids (16k p=1:
+    // ~1140 vs ~1040 TF/s).  The two are bitwise identical, so the choice never changes a row.
+    // KVP_ATTN_TB=0 / 1 forces either.
     static const int tb = [] {
         const char* e = getenv("KVP_ATTN_TB");
         return e ? atoi(e) : -1;
