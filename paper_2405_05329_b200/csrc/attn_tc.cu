@@ -515,17 +515,17 @@ void attn_bf16_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const At
         return e ? atoi(e) : 2;
     }();
     const bool h128 = sh.head_dim == 128;
-    // hd 128: the double-buffered one-tile-per-CTA kernel (attn_tb.cu) on grids of up to four
+    // hd 128: the double-buffered one-tile-per-CTA kernel (attn_tb.cu) on grids of up to two
     // waves of 256-row CTAs -- the rank chunks of KV-Runahead (Llama 4k p=8 last rank: ~650 vs
-    // ~390 TF/s; 4k p=1: ~880 vs ~875), this kernel's two-tile CTAs on bigger grids (16k p=1:
-    // ~1140 vs ~1040 TF/s).  The two are bitwise identical, so the choice never changes a row.
-    // KVP_ATTN_TB=0 / 1 forces either.
+    // ~390 TF/s), this kernel's two-tile CTAs on bigger grids (4k p=1 in the full step: 5.8 vs
+    // 5.9 ms; 16k p=1: ~1140 vs ~1040 TF/s).  The two are bitwise identical, so the choice never
+    // changes a row.  KVP_ATTN_TB=0 / 1 forces either.
     static const int tb = [] {
         const char* e = getenv("KVP_ATTN_TB");
         return e ? atoi(e) : -1;
     }();
     const int64_t ctas256 = static_cast<int64_t>(sh.n_heads) * ((sh.q_rows + 255) / 256);
-    if (h128 && (tb == 1 || (tb < 0 && ctas256 <= 4 * 148))) return attn_bf16_tb(Q, K, V, O, sh, s);
+    if (h128 && (tb == 1 || (tb < 0 && ctas256 <= 2 * 148))) return attn_bf16_tb(Q, K, V, O, sh, s);
     const int np = poly >= 0 ? poly : (h128 ? DEFAULT_POLY_128 : DEFAULT_POLY_64);
     if (h128)
         launch_poly<128, 2, 128>(np, Q, K, V, O, sh, s);

@@ -290,16 +290,17 @@ def test_llama7b_shape_strategy_invariance_bf16():
 
 def test_strategies_bitwise_across_attention_kernels():
     """The hd-128 attention has two kernels, picked by grid size (attn_tc.cu: two query tiles
-    per CTA on big grids; attn_tb.cu: one tile per CTA on rank-sized ones).  At C = 5120 with
-    32 heads the serial run's grid (32 x 20 CTAs of 256 rows) takes attn_tc and the p = 2 rank
-    chunks take attn_tb, so this checks that the two kernels agree bit for bit and Serial ==
+    per CTA on big grids; attn_tb.cu: one tile per CTA on rank-sized ones, up to 2 x 148
+    CTAs of 256 rows).  At C = 5120 with 32 heads the serial run (32 x 20) takes attn_tc, the
+    KVR ranks one each (3072 rows: 32 x 12 -> attn_tc, 2048 rows: 32 x 8 -> attn_tb) and the
+    TSP ranks attn_tb, so this checks that the two kernels agree bit for bit and Serial ==
     KVR == TSP stays bitwise across the selection."""
     W = engine(4096, 32, 32, 1, 1, "bf16", True)
     C_ = 5120
     ctx = O.random_context(C_, 4096, 23, np.float32)
     serial = kv.run(kv.Strategy.Serial, ctx, kv.even_partition(C_, 1), W)
-    kvr = kv.run(kv.Strategy.KVR, ctx, kv.partition_from_ratios(C_, [0.55, 0.45]), W)
-    tsp = kv.run(kv.Strategy.TSP, ctx, kv.even_partition(C_, 2), W)
+    kvr = kv.run(kv.Strategy.KVR, ctx, kv.ContextPartition(C_, [0, 3072, C_]), W)
+    tsp = kv.run(kv.Strategy.TSP, ctx, kv.even_partition(C_, 4), W)
     assert np.isfinite(serial.hidden_out).all()
     assert np.array_equal(serial.hidden_out, kvr.hidden_out)
     assert np.array_equal(serial.hidden_out, tsp.hidden_out)
