@@ -1,5 +1,5 @@
 // attn_tb.cu -- prefix-causal flash attention with the score tile triple-buffered in tensor
-// memory (tcgen05, one 128-query tile per CTA); head_dim 128.
+// memory (tcgen05, one 128-query tile per CTA); head_dim 128 or 64.
 //
 // Reference: causal_attention (model.hpp:112-158).  A CTA owns 128 query rows of one head and
 // walks the 128-key tiles [0, offset + last query]:
@@ -39,22 +39,26 @@ bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t 
 namespace {
 using namespace smx;
 
-constexpr int HD = 128;
 constexpr int BQ = 128;  // query rows per CTA
 constexpr int BK = 128;  // keys per tile
 constexpr int NS = 2;    // S buffers (and P buffers)
-constexpr int KST = 3, VST = 2;
 constexpr int THREADS = 352;  // 11 warps
-constexpr uint32_t Q_BYTES = BQ * HD * 2;            // 32 KB: two 64-dim SW128 boxes
-constexpr uint32_t KV_BYTES = BK * HD * 2;           // 32 KB: 128 keys x 128 dims (two 64-dim boxes)
 constexpr uint32_t P_COL = NS * BK;                  // P_0 | P_1 at TMEM columns 256, 320 (bf16 packed)
-constexpr uint32_t O_COL = P_COL + NS * BK / 2;      // O at TMEM column 384
+constexpr uint32_t O_COL = P_COL + NS * BK / 2;      // O at TMEM column 384 (HD columns)
 constexpr uint32_t BAR_BYTES = 256;
-constexpr uint32_t XCH_BYTES = 5 * BQ * 4;  // running row max handed between the sets + epilogue l, m
-constexpr uint32_t NEED = Q_BYTES + (KST + VST) * KV_BYTES + BAR_BYTES + XCH_BYTES;
-constexpr uint32_t SMEM = NEED + 1024;
-static_assert(SMEM <= 232448, "attention smem over the 227 KB opt-in limit");
+constexpr uint32_t XCH_BYTES = 5 * BQ * 4;  // running row max handed between the sets + row sums
 constexpr float RESCALE_THRESHOLD = 8.0f;
+// head_dim 128 (Llama) or 64 (Falcon): Q / K / V tiles are HD / 64 SW128 boxes of 64 dims
+template <int HD>
+struct TbCfg {
+    static constexpr int KST = HD == 128 ? 3 : 4, VST = HD == 128 ? 2 : 3;
+    static constexpr uint32_t Q_BYTES = BQ * HD * 2;   // 32 / 16 KB
+    static constexpr uint32_t KV_BYTES = BK * HD * 2;  // 32 / 16 KB
+    static constexpr uint32_t NEED = Q_BYTES + (KST + VST) * KV_BYTES + BAR_BYTES + XCH_BYTES;
+    static constexpr uint32_t SMEM = NEED + 1024;
+    static_assert(SMEM <= 232448, "attention smem over the 227 KB opt-in limit");
+    static_assert(O_COL + HD <= 512, "TMEM holds S x 2, P x 2 and O");
+};
 
 struct PairArgs {
     int64_t q_rows, offset;
@@ -80,10 +84,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-template <int NPOLY>
+template <int HD, int NPOLY>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_tb_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, PairArgs a) {
+    using TC = TbCfg<HD>;
+    constexpr int KST = TC::KST, VST = TC::VST;
+    constexpr uint32_t Q_BYTES = TC::Q_BYTES, KV_BYTES = TC::KV_BYTES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t pad = (1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u;
     uint8_t* smem = smem_raw + pad;
@@ -155,14 +162,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         // the next K behind it (measured: the S issue then trails PV completion + a TMA round trip)
         if (lane == 0) {
             ptx::mbar_arrive_expect_tx(q_full, Q_BYTES);
-            for (int hv = 0; hv < 2; ++hv)
+            for (int hv = 0; hv < HD / 64; ++hv)
                 ptx::tma_load_2d(sQ + hv * BQ * 128, &tmQ, q_full, h * HD + hv * 64, static_cast<int32_t>(q0));
             for (int t = 0; t < n; ++t) {
                 const int sk = t % KST;
                 ptx::mbar_wait(&k_empty[sk], ((t / KST) & 1) ^ 1);
                 TB_TRACE(8, t);
                 ptx::mbar_arrive_expect_tx(&k_full[sk], KV_BYTES);
-                for (int hv = 0; hv < 2; ++hv)
+                for (int hv = 0; hv < HD / 64; ++hv)
                     ptx::tma_load_2d(sK + sk * KV_BYTES + hv * BK * 128, &tmK, &k_full[sk], g * HD + hv * 64, t * BK);
             }
         }
@@ -173,7 +180,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 ptx::mbar_wait(&v_empty[sv], ((t / VST) & 1) ^ 1);
                 TB_TRACE(9, t);
                 ptx::mbar_arrive_expect_tx(&v_full[sv], KV_BYTES);
-                for (int hv = 0; hv < 2; ++hv)
+                for (int hv = 0; hv < HD / 64; ++hv)
                     ptx::tma_load_2d(sV + sv * KV_BYTES + hv * BK * 128, &tmV, &v_full[sv], g * HD + hv * 64, t * BK);
             }
         }
@@ -378,11 +385,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         const float inv = 1.0f / xl[((n - 1) & 1) * BQ + xrow];
         ptx::mbar_wait(o_final, 0);
         ptx::tc_fence_after();
-        bf16* orow = a.O + row * a.ldo + static_cast<int64_t>(h) * HD + set * 64;
+        bf16* orow = a.O + row * a.ldo + static_cast<int64_t>(h) * HD + set * (HD / 2);
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
+        for (int c = 0; c < HD / 64; ++c) {
             uint32_t r[32];
-            ptx::tmem_ld32(lane_base + O_COL + set * 64 + c * 32, r);
+            ptx::tmem_ld32(lane_base + O_COL + set * (HD / 2) + c * 32, r);
             ptx::tmem_ld_wait();
             if (row < a.q_rows) {
 #pragma unroll
@@ -414,14 +421,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 }
 
-template <int NPOLY>
+template <int HD, int NPOLY>
 void launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShape& sh, cudaStream_t s) {
+    constexpr uint32_t SMEM = TbCfg<HD>::SMEM;
     CUtensorMap tq, tk, tv;
     if (!make_tmap_bf16(&tq, Q, static_cast<uint64_t>(sh.n_heads) * HD, sh.q_rows, sh.ldq, 64, BQ) ||
         !make_tmap_bf16(&tk, K, static_cast<uint64_t>(sh.n_kv_heads) * HD, sh.k_rows, sh.ldkv, 64, BK) ||
         !make_tmap_bf16(&tv, V, static_cast<uint64_t>(sh.n_kv_heads) * HD, sh.k_rows, sh.ldkv, 64, BK))
         throw std::runtime_error("attn_tb: cuTensorMapEncodeTiled failed");
-    auto kern = attn_tb_kernel<NPOLY>;
+    auto kern = attn_tb_kernel<HD, NPOLY>;
     static thread_local int configured = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -489,18 +497,18 @@ void launch(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShap
 
 void attn_bf16_tb(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const AttnShape& sh, cudaStream_t s) {
     if (sh.q_rows <= 0) return;
-    if (sh.head_dim != HD) throw std::runtime_error("attn_tb: head_dim must be 128");
+    if (sh.head_dim != 128 && sh.head_dim != 64) throw std::runtime_error("attn_tb: head_dim must be 64 or 128");
     if (sh.offset + sh.q_rows + 2 * BQ >= (int64_t(1) << 31)) throw std::runtime_error("attn_tb: positions must be < 2^31");
     static const int poly = [] {
         const char* e = getenv("KVP_ATTN_POLY");
         return e ? atoi(e) : 0;
     }();
+    const bool h128 = sh.head_dim == 128;
     switch (poly) {
-        case 0: launch<0>(Q, K, V, O, sh, s); break;
-        case 2: launch<2>(Q, K, V, O, sh, s); break;
-        case 4: launch<4>(Q, K, V, O, sh, s); break;
-        case 6: launch<6>(Q, K, V, O, sh, s); break;
-        default: throw std::runtime_error("attn_tb: KVP_ATTN_POLY must be 0, 2, 4 or 6");
+        case 0: h128 ? launch<128, 0>(Q, K, V, O, sh, s) : launch<64, 0>(Q, K, V, O, sh, s); break;
+        case 2: h128 ? launch<128, 2>(Q, K, V, O, sh, s) : launch<64, 2>(Q, K, V, O, sh, s); break;
+        case 4: h128 ? launch<128, 4>(Q, K, V, O, sh, s) : launch<64, 4>(Q, K, V, O, sh, s); break;
+        default: throw std::runtime_error("attn_tb: KVP_ATTN_POLY must be 0, 2 or 4");
     }
 }
 

@@ -525,7 +525,11 @@ void attn_bf16_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const At
         return e ? atoi(e) : -1;
     }();
     const int64_t ctas256 = static_cast<int64_t>(sh.n_heads) * ((sh.q_rows + 255) / 256);
-    if (h128 && (tb == 1 || (tb < 0 && ctas256 <= 2 * 148))) return attn_bf16_tb(Q, K, V, O, sh, s);
+    // hd 64 (Falcon) the same way, while this kernel runs its default two 128-key tiles -- the
+    // layout attn_tb restates bit for bit (isolated: Falcon p = 4 / 8 rank chunks 621 / 607 vs
+    // 596 / 578 TF/s; the full 8k grid is a tie in the power-capped step)
+    const bool tb_ok = h128 || hd64_tiles == 2;
+    if (tb_ok && (tb == 1 || (tb < 0 && ctas256 <= 2 * 148))) return attn_bf16_tb(Q, K, V, O, sh, s);
     const int np = poly >= 0 ? poly : (h128 ? DEFAULT_POLY_128 : DEFAULT_POLY_64);
     if (h128)
         launch_poly<128, 2, 128>(np, Q, K, V, O, sh, s);

@@ -11,6 +11,7 @@ from paper_2405_05329_b200 import kvprefill as kv  # noqa: E402
 SHAPES = {  # name: (q_rows, offset, heads, kv_heads, head_dim)
     "llama_4k": (4096, 0, 32, 32, 128), "llama_16k": (16384, 0, 32, 32, 128),
     "llama_4k_p8_last": (512, 3584, 32, 32, 128), "llama_16k_p8_last": (2048, 14336, 32, 32, 128), "falcon_8k": (8192, 0, 71, 1, 64),
+    "falcon_8k_p8_last": (1024, 7168, 71, 1, 64), "falcon_8k_p4_last": (2048, 6144, 71, 1, 64),
 }
 W = kv.init_weights(kv.ModelConfig(256, 2, 2, 1, 1, "bf16", False))
 tag = ",".join(f"{k[9:]}={v}" for k, v in sorted(os.environ.items()) if k.startswith("KVP_ATTN_"))
