@@ -20,9 +20,10 @@ Hang safety of the peer-memory transport: its flag waits are enqueued on the GPU
 (cuStreamWaitValue32), so a peer that dies or never signals would block the stream for good.
 Before reading its result each rank polls its streams against a deadline
 (KVP_PEER_TIMEOUT_S, default 120 s); on expiry it writes the awaited values into its OWN flag
-words from a side stream (the stuck waits release, the stream drains), drops the peer
-mappings, and reports a ProtocolError that the post-run agreement raises on every rank -- the
-analogue of Channel::close waking blocked receivers (channel.hpp:15-18, 120-136).
+words from a side stream (the stuck waits release, the stream drains) and reports a
+ProtocolError that the post-run agreement raises on every rank, after which every rank drops
+its peer session -- the analogue of Channel::close waking blocked receivers
+(channel.hpp:15-18, 120-136).
 """
 from __future__ import annotations
 
@@ -335,9 +336,11 @@ def _drain_or_release(executor, ps, top_value: int, timeout_s: float) -> bool:
     flag value of this run, into every flag slot from a side stream), lets the streams drain
     and returns False (the caller agrees the error and every rank drops its peer session)."""
     streams = (executor._stream, ps.comm)
-    deadline = time.monotonic() + timeout_s
+    t0 = time.monotonic()
+    deadline = t0 + timeout_s
     while not all(s.query() for s in streams):
-        if time.monotonic() > deadline:
+        now = time.monotonic()
+        if now > deadline:
             torch = executor.torch
             side = torch.cuda.Stream(device=executor.device)
             for slot in range(_FLAG_SLOTS):
@@ -346,7 +349,8 @@ def _drain_or_release(executor, ps, top_value: int, timeout_s: float) -> bool:
             for s in streams:
                 s.synchronize()
             return False
-        time.sleep(0.0005)
+        if now - t0 > 0.02:  # busy-poll the first 20 ms (the normal case), then back off
+            time.sleep(0.001)
     return True
 
 
