@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const uint64_t off_k = ((k >> 2) * (BK * 128) + (k & 3) * 32) >> 4;
                 ptx::mma_bf16_ss_w(tmem + (t % NS) * BK, qdesc + off_q, kdesc + off_k, idesc_s, k != 0);
             }
+            if (lane == 0) TB_TRACE(10, t);  // all 8 S MMAs accepted by the issue queue
             ptx::mma_commit_w(&s_full[t % NS]);
             ptx::mma_commit_w(&k_empty[s]);
         };
@@ -231,6 +232,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 ptx::mma_bf16_ts_w(tmem + O_COL, pa, vdesc + static_cast<uint64_t>((k * 16 * 128) >> 4), idesc_o,
                                    (j | k) != 0);
             }
+            if (lane == 0) TB_TRACE(11, j);  // all 8 PV MMAs accepted
             ptx::mma_commit_w(&o_done[j & 1]);
             ptx::mma_commit_w(&v_empty[sv]);
         }

@@ -31,3 +31,5 @@ if n > 8:
     print(f"median per key tile: PV issue period {per:.0f} clk (tensor work 1024)")
     print(f" S issue(j)->sm0 S seen(j) {d(2, 0):.0f}, S seen->xchg {d(4, 2):.0f}, xchg->P {d(6, 4):.0f}, "
           f"P(j)->PV issue(j) {d(1, 6):.0f}, sm0 P(j)->S seen(j+1) {d(2, 6, 1):.0f}")
+    if (t[10] != 0).sum() > 8:
+        print(f" issue of 8 S MMAs {d(10, 0):.0f} clk, of 8 PV MMAs {d(11, 1):.0f} clk")
