@@ -43,6 +43,9 @@ RUNS = [
     ("falcon7b-8k", "bf16", "kvr", [0.6, 0.4]),
     ("falcon7b-8k", "f32", "kvr", [1.0]),
     ("llama7b-16k", "bf16", "kvr", [1.0]),
+    # the north-star setting: KVR-S split of 16k over 8 ranks (profiles/r02/balancer_llama7b_16k.json)
+    ("llama7b-16k", "bf16", "kvr", [r / 16384 for r in (2778, 2581, 2256, 2030, 1861, 1728, 1620, 1530)]),
+    ("llama7b-16k", "bf16", "tsp", [0.125] * 8),
     ("llama7b-16k", "f32", "kvr", [1.0]),
 ]
 RUNS = [r for r in RUNS if r[0] in G]
