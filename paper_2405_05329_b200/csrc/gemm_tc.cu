@@ -477,8 +477,12 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {  // in a pair only the leader issues the MMAs
+        // in a pair only the leader issues the MMAs: the whole warp runs the loop converged and
+        // one elect.sync lane issues (ptx::*_w), descriptors advanced by constant offsets
+        if (rank == 0) {
             constexpr uint32_t idesc_w = ptx::idesc_bf16(TM, BN), idesc_n = ptx::idesc_bf16(TM, BN / 2);
+            const uint64_t adesc0 = ptx::smem_desc_sw128(ptx::smem_u32(sA), 16, 1024);
+            const uint64_t bdesc0 = ptx::smem_desc_sw128(ptx::smem_u32(sB), 16, 1024);
             int stage = 0;
             uint32_t phase = 0;
             int t = 0;
@@ -493,30 +497,30 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (int kb = 0; kb < num_kb; ++kb) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
-                    const uint32_t a0 = ptx::smem_u32(sA + stage * C::A_BYTES);
-                    const uint32_t b0 = ptx::smem_u32(sB + stage * C::B_BYTES);
+                    const uint64_t ad0 = adesc0 + static_cast<uint64_t>((stage * C::A_BYTES) >> 4);
+                    const uint64_t bd0 = bdesc0 + static_cast<uint64_t>((stage * C::B_BYTES) >> 4);
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k) {
-                        const uint64_t ad = ptx::smem_desc_sw128(a0 + k * 32, 16, 1024);
-                        const uint64_t bd = ptx::smem_desc_sw128(b0 + k * 32, 16, 1024);
+                        const uint64_t ad = ad0 + static_cast<uint64_t>((k * 32) >> 4);
+                        const uint64_t bd = bd0 + static_cast<uint64_t>((k * 32) >> 4);
                         if constexpr (NCTA == 2)
-                            ptx::mma_bf16_ss_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                            ptx::mma_bf16_ss_pair_w(d_tmem, ad, bd, idesc, (kb | k) != 0);
                         else
-                            ptx::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                            ptx::mma_bf16_ss_w(d_tmem, ad, bd, idesc, (kb | k) != 0);
                     }
                     if constexpr (NCTA == 2)
-                        ptx::mma_commit_pair(&empty[stage], 0x3);
+                        ptx::mma_commit_pair_w(&empty[stage], 0x3);
                     else
-                        ptx::mma_commit(&empty[stage]);
+                        ptx::mma_commit_w(&empty[stage]);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
                 if constexpr (NCTA == 2)
-                    ptx::mma_commit_pair(&tfull[buf], 0x3);
+                    ptx::mma_commit_pair_w(&tfull[buf], 0x3);
                 else
-                    ptx::mma_commit(&tfull[buf]);
+                    ptx::mma_commit_w(&tfull[buf]);
             }
         }
     } else {
