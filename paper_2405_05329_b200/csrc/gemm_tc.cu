@@ -118,7 +118,6 @@ struct EpiArgs {
     int rope_hd;  // EPI_ROPE kinds: GemmEpilogue::rope_*
     int64_t rope_pos0;
     const float* rope_inv_freq;
-    int l2_hints;  // TMA L2 policies for A / B (KVP_GEMM_L2HINT=1..3; off by default)
 };
 
 // EPI_QKV / EPI_QKV_MIRROR | EPI_ROPE: the same epilogue with the rotary embedding applied to
@@ -427,52 +426,35 @@ __global__ void __launch_bounds__(THREADS, 1)
     ptx::griddep_wait();
 
     if (warp == 0) {
-        if (lane == 0) {
-            // the raster group's A rows are re-read for every column block: keep them in L2;
-            // a B column block is read by the group's tiles in flight at the same time
-            // (KVP_GEMM_L2HINT: 1 A last / B first, 2 A last only, 3 B last only)
-            const uint64_t pol_norm = ptx::policy_evict_normal();
-            const uint64_t pol_a = ep.l2_hints == 3 ? pol_norm : ptx::policy_evict_last();
-            const uint64_t pol_b = ep.l2_hints == 1 ? ptx::policy_evict_first()
-                                                    : (ep.l2_hints == 3 ? ptx::policy_evict_last() : pol_norm);
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int tile = unit; tile < num_tiles; tile += n_units) {
-                int m_blk, col_base, width;
-                decode(tile, m_blk, col_base, width);
-                const bool narrow = width != BN;
-                const uint32_t bytes = C::A_BYTES + (narrow ? C::B_BYTES / 2 : C::B_BYTES);
-                const int a_row = m_blk * TM + static_cast<int>(rank) * BM;
-                const int b_row = col_base + static_cast<int>(rank) * (width / NCTA);
-                for (int kb = 0; kb < num_kb; ++kb) {
-                    ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    if constexpr (NCTA == 2) {
-                        // both CTAs' bytes land on the leader's stage barrier
-                        if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * bytes);
-                        const uint32_t bar = ptx::cluster_addr(&full[stage], 0);
-                        if (ep.l2_hints) {
-                            ptx::tma_load_2d_pair_hint(sA + stage * C::A_BYTES, &tmA, bar, kb * BK, a_row, pol_a);
-                            ptx::tma_load_2d_pair_hint(sB + stage * C::B_BYTES, narrow ? &tmBh : &tmB, bar, kb * BK,
-                                                       b_row, pol_b);
-                        } else {
-                            ptx::tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, bar, kb * BK, a_row);
-                            ptx::tma_load_2d_pair(sB + stage * C::B_BYTES, narrow ? &tmBh : &tmB, bar, kb * BK, b_row);
-                        }
-                    } else {
-                        ptx::mbar_arrive_expect_tx(&full[stage], bytes);
-                        if (ep.l2_hints) {
-                            ptx::tma_load_2d_hint(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, a_row, pol_a);
-                            ptx::tma_load_2d_hint(sB + stage * C::B_BYTES, narrow ? &tmBh : &tmB, &full[stage], kb * BK,
-                                                  b_row, pol_b);
-                        } else {
-                            ptx::tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, a_row);
-                            ptx::tma_load_2d(sB + stage * C::B_BYTES, narrow ? &tmBh : &tmB, &full[stage], kb * BK, b_row);
-                        }
-                    }
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+        // TMA producer: the whole warp runs the loop converged; one elect.sync lane arms the
+        // stage barrier and issues the loads (ptx::*_w).  (L2 cache policies on these loads
+        // -- evict_last A / evict_first B, or either alone -- were measured and did not help,
+        // profiles/r02/gemm_l2hint.txt.)
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = unit; tile < num_tiles; tile += n_units) {
+            int m_blk, col_base, width;
+            decode(tile, m_blk, col_base, width);
+            const bool narrow = width != BN;
+            const uint32_t bytes = C::A_BYTES + (narrow ? C::B_BYTES / 2 : C::B_BYTES);
+            const int a_row = m_blk * TM + static_cast<int>(rank) * BM;
+            const int b_row = col_base + static_cast<int>(rank) * (width / NCTA);
+            for (int kb = 0; kb < num_kb; ++kb) {
+                ptx::mbar_wait(&empty[stage], phase ^ 1);
+                if constexpr (NCTA == 2) {
+                    // both CTAs' bytes land on the leader's stage barrier
+                    if (rank == 0) ptx::mbar_arrive_expect_tx_w(&full[stage], 2 * bytes);
+                    const uint32_t bar = ptx::cluster_addr(&full[stage], 0);
+                    ptx::tma_load_2d_pair_w(sA + stage * C::A_BYTES, &tmA, bar, kb * BK, a_row);
+                    ptx::tma_load_2d_pair_w(sB + stage * C::B_BYTES, narrow ? &tmBh : &tmB, bar, kb * BK, b_row);
+                } else {
+                    ptx::mbar_arrive_expect_tx_w(&full[stage], bytes);
+                    ptx::tma_load_2d_w(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, a_row);
+                    ptx::tma_load_2d_w(sB + stage * C::B_BYTES, narrow ? &tmBh : &tmB, &full[stage], kb * BK, b_row);
+                }
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
         }
@@ -665,12 +647,7 @@ void dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& t
               const GemmEpilogue& g, cudaStream_t s) {
     EpiArgs ep{g.out0, g.ld0, g.n0, g.out1, g.ld1, g.n1, g.out2, g.ld2, g.outf, g.ldf, g.resid, g.ldr,
                g.outb, g.ldb, g.ssq_out, g.ssq_in, g.ssq_parts, g.norm_cols ? 1.0f / static_cast<float>(g.norm_cols) : 0.f,
-               {}, {}, g.kind == EPI_QKV ? g.n_mirror : 0, g.rope_hd, g.rope_pos0, g.rope_inv_freq, 0};
-    static const int l2_hints = [] {
-        const char* e = getenv("KVP_GEMM_L2HINT");  // measured: no variant helps (profiles/r02)
-        return e ? atoi(e) : 0;
-    }();
-    ep.l2_hints = l2_hints;
+               {}, {}, g.kind == EPI_QKV ? g.n_mirror : 0, g.rope_hd, g.rope_pos0, g.rope_inv_freq};
     for (int m = 0; m < ep.n_mirror; ++m) {
         ep.mk[m] = g.mirror_k[m];
         ep.mv[m] = g.mirror_v[m];
