@@ -160,29 +160,25 @@ __global__ void __launch_bounds__(THREADS, 1)
         // K producer: Q, then K_t as soon as S_{t-KST} has read its stage.  V has its own
         // producer (warp 10): a V stage waits for PV_{t-VST}, and a single producer would hold
         // the next K behind it (measured: the S issue then trails PV completion + a TMA round trip)
-        if (lane == 0) {
-            ptx::mbar_arrive_expect_tx(q_full, Q_BYTES);
+        ptx::mbar_arrive_expect_tx_w(q_full, Q_BYTES);
+        for (int hv = 0; hv < HD / 64; ++hv)
+            ptx::tma_load_2d_w(sQ + hv * BQ * 128, &tmQ, q_full, h * HD + hv * 64, static_cast<int32_t>(q0));
+        for (int t = 0; t < n; ++t) {
+            const int sk = t % KST;
+            ptx::mbar_wait(&k_empty[sk], ((t / KST) & 1) ^ 1);
+            TB_TRACE(8, t);
+            ptx::mbar_arrive_expect_tx_w(&k_full[sk], KV_BYTES);
             for (int hv = 0; hv < HD / 64; ++hv)
-                ptx::tma_load_2d(sQ + hv * BQ * 128, &tmQ, q_full, h * HD + hv * 64, static_cast<int32_t>(q0));
-            for (int t = 0; t < n; ++t) {
-                const int sk = t % KST;
-                ptx::mbar_wait(&k_empty[sk], ((t / KST) & 1) ^ 1);
-                TB_TRACE(8, t);
-                ptx::mbar_arrive_expect_tx(&k_full[sk], KV_BYTES);
-                for (int hv = 0; hv < HD / 64; ++hv)
-                    ptx::tma_load_2d(sK + sk * KV_BYTES + hv * BK * 128, &tmK, &k_full[sk], g * HD + hv * 64, t * BK);
-            }
+                ptx::tma_load_2d_w(sK + sk * KV_BYTES + hv * BK * 128, &tmK, &k_full[sk], g * HD + hv * 64, t * BK);
         }
     } else if (warp == 10) {
-        if (lane == 0) {
-            for (int t = 0; t < n; ++t) {
-                const int sv = t % VST;
-                ptx::mbar_wait(&v_empty[sv], ((t / VST) & 1) ^ 1);
-                TB_TRACE(9, t);
-                ptx::mbar_arrive_expect_tx(&v_full[sv], KV_BYTES);
-                for (int hv = 0; hv < HD / 64; ++hv)
-                    ptx::tma_load_2d(sV + sv * KV_BYTES + hv * BK * 128, &tmV, &v_full[sv], g * HD + hv * 64, t * BK);
-            }
+        for (int t = 0; t < n; ++t) {
+            const int sv = t % VST;
+            ptx::mbar_wait(&v_empty[sv], ((t / VST) & 1) ^ 1);
+            TB_TRACE(9, t);
+            ptx::mbar_arrive_expect_tx_w(&v_full[sv], KV_BYTES);
+            for (int hv = 0; hv < HD / 64; ++hv)
+                ptx::tma_load_2d_w(sV + sv * KV_BYTES + hv * BK * 128, &tmV, &v_full[sv], g * HD + hv * 64, t * BK);
         }
     } else if (warp == 1) {
         // the whole warp runs the issue loop converged; one elected lane issues each

@@ -166,30 +166,28 @@ __global__ void __launch_bounds__(threads_for<NT>(), 1)
     ptx::griddep_wait();
 
     if (warp == 0) {
-        if (lane == 0) {
-            ptx::mbar_arrive_expect_tx(q_full, NT * C::Q_BYTES);
-            for (int x = 0; x < NT; ++x)
-                for (int hv = 0; hv < C::HALVES; ++hv)
-                    ptx::tma_load_2d(sQ + x * C::Q_BYTES + hv * BQ * 128, &tmQ, q_full, h * HD + hv * 64,
-                                     static_cast<int32_t>(q0 + x * BQ));
-            // K(t), V(t) in need order; K(t) waits for the S MMAs of key tile t - KST, V(t) for
-            // its PV MMAs, so K runs a stage further ahead (blocking waits: the producer lane
-            // never spins on the issue slots of the softmax warps of its SMSP)
-            for (int t = 0; t < n_kt[NT - 1]; ++t) {
-                const int sk = t % KST, sv = t % VST;
-                ptx::mbar_wait(&k_empty[sk], ((t / KST) & 1) ^ 1);
-                ATTN_TRACE(12, t);
-                ptx::mbar_arrive_expect_tx(&k_full[sk], C::KV_BYTES);
-                for (int hv = 0; hv < C::HALVES; ++hv)
-                    ptx::tma_load_2d(sK + sk * C::KV_BYTES + hv * BKV * 128, &tmK, &k_full[sk], g * HD + hv * 64,
-                                     t * BKV);
-                ptx::mbar_wait(&v_empty[sv], ((t / VST) & 1) ^ 1);
-                ATTN_TRACE(13, t);
-                ptx::mbar_arrive_expect_tx(&v_full[sv], C::KV_BYTES);
-                for (int hv = 0; hv < C::HALVES; ++hv)
-                    ptx::tma_load_2d(sV + sv * C::KV_BYTES + hv * BKV * 128, &tmV, &v_full[sv], g * HD + hv * 64,
-                                     t * BKV);
-            }
+        ptx::mbar_arrive_expect_tx_w(q_full, NT * C::Q_BYTES);
+        for (int x = 0; x < NT; ++x)
+            for (int hv = 0; hv < C::HALVES; ++hv)
+                ptx::tma_load_2d_w(sQ + x * C::Q_BYTES + hv * BQ * 128, &tmQ, q_full, h * HD + hv * 64,
+                                 static_cast<int32_t>(q0 + x * BQ));
+        // K(t), V(t) in need order; K(t) waits for the S MMAs of key tile t - KST, V(t) for
+        // its PV MMAs, so K runs a stage further ahead (blocking waits: the producer lane
+        // never spins on the issue slots of the softmax warps of its SMSP)
+        for (int t = 0; t < n_kt[NT - 1]; ++t) {
+            const int sk = t % KST, sv = t % VST;
+            ptx::mbar_wait(&k_empty[sk], ((t / KST) & 1) ^ 1);
+            ATTN_TRACE(12, t);
+            ptx::mbar_arrive_expect_tx_w(&k_full[sk], C::KV_BYTES);
+            for (int hv = 0; hv < C::HALVES; ++hv)
+                ptx::tma_load_2d_w(sK + sk * C::KV_BYTES + hv * BKV * 128, &tmK, &k_full[sk], g * HD + hv * 64,
+                                 t * BKV);
+            ptx::mbar_wait(&v_empty[sv], ((t / VST) & 1) ^ 1);
+            ATTN_TRACE(13, t);
+            ptx::mbar_arrive_expect_tx_w(&v_full[sv], C::KV_BYTES);
+            for (int hv = 0; hv < C::HALVES; ++hv)
+                ptx::tma_load_2d_w(sV + sv * C::KV_BYTES + hv * BKV * 128, &tmV, &v_full[sv], g * HD + hv * 64,
+                                 t * BKV);
         }
     } else if (warp == 1) {
         // the whole warp runs the issue loop converged; one elected lane issues each
