@@ -1,27 +1,26 @@
-// attn_tb.cu -- prefix-causal flash attention with the score tile triple-buffered in tensor
-// memory (tcgen05, one 128-query tile per CTA); head_dim 128 or 64.
+// attn_tb.cu -- prefix-causal flash attention with the score tile and P double-buffered in
+// tensor memory (tcgen05, one 128-query tile per CTA); head_dim 128 or 64.
 //
 // Reference: causal_attention (model.hpp:112-158).  A CTA owns 128 query rows of one head and
 // walks the 128-key tiles [0, offset + last query]:
-//   S_j  = Q K_j^T   (SS MMA, M = N = 128)  -> S buffer j % 3 in TMEM
-//   O   += P_j V_j   (TS MMA: A = P_j packed in TMEM over S_j, B = V_j MN-major)
-// With three S buffers the MMA issuer computes S_{j+2} before it waits for P_j: the scores of
-// the next tiles never wait for the softmax, and the softmax warps find S_{j+1} ready when they
-// finish P_j.  The per-step chain S -> softmax -> PV -> S of a kernel whose P aliases its only
-// S buffer (attn_tc.cu: two query tiles ping-pong, each chain ~3.4k clk for 1k clk of its own
-// MMAs) is gone; the tensor pipe and the softmax run concurrently at their own rates.
-// TMEM (512 columns): S_0 | S_1 (128 f32 columns each) | P_0 | P_1 (64 columns each, bf16
-// packed) | O (128 columns).
-// Warps: 0 TMA producer (Q, K), 10 TMA producer (V), 1 MMA issuer + TMEM owner, 2..9 softmax
-// in two sets (even / odd key tiles, one thread per query row each; warp w reads TMEM lane
-// quarter w % 4): the running row max is handed between the sets once per tile, so each SMSP
-// has two softmax warps in different phases of consecutive tiles feeding its MUFU.  O is rescaled in
-// TMEM only when a row max grows by more than 2^8, exactly as in attn_tc.cu; key tiles are
-// aligned to absolute key 0 and rows are independent, so results do not depend on how the
-// context is split over ranks.
-// (A CTA-pair variant -- cta_group::2, M = 256, each SM loading half of every K/V tile -- was
-// measured first: its N = 128 pair MMAs execute at ~40 % of the single-CTA rate, 2.5k clk per
-// key step for 1k clk of work, profiles/r02/README.md.)
+//   S_j  = Q K_j^T   (SS MMA, M = N = 128)  -> S buffer j % 2 in TMEM
+//   O   += P_j V_j   (TS MMA: A = P_j, bf16 packed in P buffer j % 2; B = V_j MN-major)
+// The MMA issuer computes S_{j+2} as soon as the softmax has read S_j into registers
+// (`s_free`), and PV_j when P_j lands: the scores of the next tiles never wait for the
+// softmax.  (In attn_tc.cu P aliases its tile's only S buffer, so each query tile runs the
+// chain S -> softmax -> PV -> S, ~3.4k clk for 1k clk of its own MMAs.)
+// TMEM (512 columns): S_0 | S_1 (128 f32 columns each) | P_0 | P_1 (64 columns each) | O (HD).
+// Warps: 0 TMA producer (Q, K), 10 TMA producer (V), 1 MMA issuer + TMEM owner (all three run
+// converged; one elect.sync lane issues), 2..9 softmax in two sets (set j % 2 owns key tile j,
+// one thread per query row; warp w reads TMEM lane quarter w % 4).  The running row max and
+// the row sum are handed between the sets in tile order, so each SMSP has two softmax warps in
+// different phases of consecutive tiles feeding its MUFU, and every row gets exactly
+// attn_tc.cu's operations in attn_tc.cu's order -- the two kernels are bitwise identical, and
+// which one a rank's grid selects never changes a result.  O is rescaled in TMEM only when a
+// row max grows by more than 2^8; key tiles are aligned to absolute key 0 and rows are
+// independent, so results do not depend on how the context is split over ranks.
+// (Variants measured and not kept -- CTA pairs, three sets, two threads per row, two issuing
+// warps, a persistent grid, FMA-pipe exp2: profiles/r02/README.md.)
 #include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
