@@ -700,8 +700,9 @@ int gemm_bf16_tc_bn(int64_t M, int64_t N) {
         const double useful = static_cast<double>(M) * N / (static_cast<double>(waves) * units * tm * bn);
         return useful * tile_eff;
     };
-    // per-FLOP efficiency of the narrow tile relative to BN=256 (measured)
-    bool wide = score(256, 1.0) >= score(128, pair ? 0.65 : 0.72);
+    // per-FLOP efficiency of the narrow tile relative to BN=256 (measured; the narrow pair
+    // tile went from 0.65 to ~0.8 with the converged MMA issue, profiles/r02/gemm_bn.txt)
+    bool wide = score(256, 1.0) >= score(128, pair ? 0.8 : 0.72);
     if (N < 256) wide = false;
     if (forced == 128) wide = false;
     if (forced == 256 && N >= 256) wide = true;
