@@ -330,21 +330,22 @@ def _silent_rank() -> int:
     return int(os.environ.get("KVP_PEER_SILENT_RANK", "-1"))
 
 
-def _drain_or_release(executor, ps, top_value: int, timeout_s: float) -> bool:
+def _drain_or_release(executor, ps, top_value: int, timeout_s: float, side_stream=None,
+                      signal=None) -> bool:
     """Waits until the rank's compute and comm streams are idle.  True if they drained in
     time; otherwise releases the rank's own stuck flag waits (writes top_value, the largest
     flag value of this run, into every flag slot from a side stream), lets the streams drain
-    and returns False (the caller agrees the error and every rank drops its peer session)."""
+    and returns False (the caller agrees the error and every rank drops its peer session).
+    side_stream / signal: injectable for tests (default: a fresh CUDA stream, _signal)."""
     streams = (executor._stream, ps.comm)
     t0 = time.monotonic()
     deadline = t0 + timeout_s
     while not all(s.query() for s in streams):
         now = time.monotonic()
         if now > deadline:
-            torch = executor.torch
-            side = torch.cuda.Stream(device=executor.device)
+            side = side_stream() if side_stream else executor.torch.cuda.Stream(device=executor.device)
             for slot in range(_FLAG_SLOTS):
-                _signal(side.cuda_stream, ps.my_flag(slot), top_value)
+                (signal or _signal)(side.cuda_stream, ps.my_flag(slot), top_value)
             side.synchronize()
             for s in streams:
                 s.synchronize()

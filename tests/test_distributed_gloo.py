@@ -140,3 +140,48 @@ def test_world2_even_and_skewed_f32():
         strat = kv.Strategy.KVR if sc["strategy"] == "kvr" else kv.Strategy.TSP
         assert m["dot_products"] == [x * 2 for x in kv.dot_product_counts(strat, part)]
         assert sum(m["kv_pairs_sent"]) == 2 * kv.traffic_pairs(strat, part)
+
+
+def test_peer_watchdog_releases_own_flags_after_timeout():
+    """Host side of the peer-transport watchdog (distributed._drain_or_release) without a GPU:
+    streams that never drain are given up on after the timeout; the rank then writes the run's
+    largest flag value into every one of its OWN flag slots from a side stream (releasing its
+    stuck GPU-side waits), lets its streams drain and reports False; streams that drain in time
+    report True and signal nothing."""
+    import paper_2405_05329_b200.distributed as D
+
+    class Stream:
+        def __init__(self, done_after=None):
+            self.polls, self.done_after, self.synced = 0, done_after, False
+            self.cuda_stream = 1234
+
+        def query(self):
+            self.polls += 1
+            return self.done_after is not None and self.polls > self.done_after
+
+        def synchronize(self):
+            self.synced = True
+
+    class Executor:
+        def __init__(self, s):
+            self._stream = s
+
+    class Session:
+        def __init__(self, c):
+            self.comm = c
+
+        def my_flag(self, slot):
+            return 0x1000 + 4 * slot
+
+    sent = []
+    side = Stream()
+    stuck_comp, stuck_comm = Stream(), Stream()
+    ok = D._drain_or_release(Executor(stuck_comp), Session(stuck_comm), 77, 0.05,
+                             side_stream=lambda: side, signal=lambda st, flag, v: sent.append((st, flag, v)))
+    assert ok is False
+    assert sent == [(1234, 0x1000 + 4 * s, 77) for s in range(D._FLAG_SLOTS)]
+    assert side.synced and stuck_comp.synced and stuck_comm.synced
+    sent.clear()
+    assert D._drain_or_release(Executor(Stream(3)), Session(Stream(1)), 77, 5.0,
+                               side_stream=lambda: side, signal=lambda *a: sent.append(a)) is True
+    assert sent == []
