@@ -1342,9 +1342,17 @@ kvp_status kvp_bench_gemm(kvp_engine* e, int64_t M, int64_t N, int64_t K, int32_
         if (M < 1 || N < 16 || K < 8 || reps < 1) throw Error(KVP_ERR_INPUT, "bad GEMM shape");
         std::lock_guard<std::mutex> g(e->mu);
         KVP_CUDA(cudaSetDevice(e->devices[0]));
+        // KVP_GEMM_BENCH_CHAIN=c: time `reps` launches back to back (PDL-chained, as inside a
+        // layer step) cycling c weight copies, so the weights stream from HBM as in a real
+        // layer sequence; default: isolated launches behind a spin kernel, median
+        static const int chain = [] {
+            const char* v = getenv("KVP_GEMM_BENCH_CHAIN");
+            return v ? std::max(1, atoi(v)) : 0;
+        }();
+        const int copies = chain > 0 ? chain : 1;
         DevBuf a, b, of, ob, rf;
         a.ensure(M * K * 2, e->devices[0]);
-        b.ensure(N * K * 2, e->devices[0]);
+        b.ensure(copies * N * K * 2, e->devices[0]);
         of.ensure(M * N * 4, e->devices[0]);
         ob.ensure(M * N * 2, e->devices[0]);
         rf.ensure(M * N * 4, e->devices[0]);
@@ -1355,6 +1363,8 @@ kvp_status kvp_bench_gemm(kvp_engine* e, int64_t M, int64_t N, int64_t K, int32_
         launch_cast_bf16(tmp.as<float>(), a.as<bf16>(), M * K, st);
         launch_seeded_f32(tmp.as<float>(), N, K, 0.02, 12, st);
         launch_cast_bf16(tmp.as<float>(), b.as<bf16>(), N * K, st);
+        for (int c = 1; c < copies; ++c)
+            KVP_CUDA(cudaMemcpyAsync(b.as<bf16>() + c * N * K, b.as<bf16>(), N * K * 2, cudaMemcpyDeviceToDevice, st));
         launch_seeded_f32(rf.as<float>(), M, N, 1.0, 13, st);
         GemmEpilogue ep;
         ep.kind = epi;
@@ -1383,7 +1393,19 @@ kvp_status kvp_bench_gemm(kvp_engine* e, int64_t M, int64_t N, int64_t K, int32_
         KVP_CUDA(cudaEventCreate(&e0));
         KVP_CUDA(cudaEventCreate(&e1));
         std::vector<float> t;
-        for (int i = 0; i < reps + 1; ++i) {
+        if (chain > 0) {
+            for (int i = 0; i < copies; ++i)  // warm-up
+                gemm_bf16_tc(a.as<bf16>(), M, K, b.as<bf16>() + (i % copies) * N * K, N, ep, st);
+            KVP_CUDA(cudaEventRecord(e0, st));
+            for (int i = 0; i < reps; ++i)
+                gemm_bf16_tc(a.as<bf16>(), M, K, b.as<bf16>() + (i % copies) * N * K, N, ep, st);
+            KVP_CUDA(cudaEventRecord(e1, st));
+            KVP_CUDA(cudaEventSynchronize(e1));
+            float x = 0;
+            KVP_CUDA(cudaEventElapsedTime(&x, e0, e1));
+            t.push_back(x / reps);
+        }
+        for (int i = 0; chain == 0 && i < reps + 1; ++i) {
             launch_spin(100000, st);  // device time only: the host enqueues behind the spin
             KVP_CUDA(cudaEventRecord(e0, st));
             gemm_bf16_tc(a.as<bf16>(), M, K, b.as<bf16>(), N, ep, st);
@@ -1395,6 +1417,7 @@ kvp_status kvp_bench_gemm(kvp_engine* e, int64_t M, int64_t N, int64_t K, int32_
         }
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
+        gemm_trace_dump();
         std::sort(t.begin(), t.end());
         *ms = t[t.size() / 2];
         if (bn_out) *bn_out = gemm_bf16_tc_bn(M, N);

@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <stdexcept>
+#include <vector>
 
 #include "kernels.cuh"
 #include "ptx.cuh"
@@ -341,14 +342,23 @@ __device__ __forceinline__ void resid_ssq_flush(const EpiArgs& ep, const ResidT&
     for (int i = 0; i < 8; ++i) ss[i] = 0.f;
 }
 
+// tuning only (KVP_GEMM_TRACE=<file>): per-CTA globaltimer stamps -- 0 entry, 1 prologue done,
+// 2 previous grid complete (PDL), 3 first stage landed, 4 last MMA issued, 5 epilogue done;
+// 6 = SM id, 7 = tiles (scripts/gemm_trace.py)
+#define GT(ev)                                                                  \
+    do {                                                                        \
+        if (trace) trace[blockIdx.x * 8 + (ev)] = ptx::globaltimer();           \
+    } while (0)
+
 template <int BN, int KIND, int NCTA>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmBh, int M, int N, int K, int n_full, int group_m,
-                   EpiArgs ep) {
+                   unsigned long long* trace, EpiArgs ep) {
     using C = Cfg<BN, NCTA>;
     constexpr int STAGES = C::STAGES;
     constexpr int TM = BM * NCTA;  // rows of one (pair) tile
+    if (threadIdx.x == 0) GT(0);
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment by pointer arithmetic on the __shared__ array, so the compiler keeps
     // the shared state space (LDS/STS instead of generic loads/stores)
@@ -422,8 +432,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t tmem_base = *tmem_slot;
     // PDL: the prologue above overlapped the previous kernel's tail; no global memory is
     // touched before the previous grid has completed
+    if (threadIdx.x == 0) GT(1);
     ptx::griddep_launch_dependents();
     ptx::griddep_wait();
+    if (threadIdx.x == 0) GT(2);
 
     if (warp == 0) {
         // TMA producer: the whole warp runs the loop converged; one elect.sync lane arms the
@@ -479,6 +491,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (int kb = 0; kb < num_kb; ++kb) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
+                    if (t == 0 && kb == 0 && lane == 0) GT(3);
                     const uint64_t ad0 = adesc0 + static_cast<uint64_t>((stage * C::A_BYTES) >> 4);
                     const uint64_t bd0 = bdesc0 + static_cast<uint64_t>((stage * C::B_BYTES) >> 4);
 #pragma unroll
@@ -504,6 +517,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 else
                     ptx::mma_commit_w(&tfull[buf]);
             }
+            if (lane == 0) GT(4);
         }
     } else {
         // Epilogue warps 2..9: warp w may touch TMEM lanes [32*(w%4), 32*(w%4)+32); the two
@@ -521,31 +535,39 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int64_t row = row0 + quarter * 32 + lane;
             const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + buf * BN;
             if constexpr (KIND == EPI_RESID) {
-                // The residual does not depend on the accumulator: fetch the first chunk of it
-                // while the tile's MMAs are still running, then one chunk ahead.
+                // The residual does not depend on the accumulator: fetch its first two chunks
+                // while the tile's MMAs are still running, then keep two chunks in flight
+                // (the last tile's epilogue of a small-M GEMM is fully exposed).
                 const ResidT rt{row0 + quarter * 32, lane >> 3, lane & 7};
                 float* stg = reinterpret_cast<float*>(smem + STAGES * C::STAGE_BYTES + 256) + (warp - 2) * 1024;
-                float4 rv[8];
+                float4 rva[8], rvb[8];
                 float ss[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) ss[i] = 0.f;
-                resid_fetch(ep, rt, static_cast<int64_t>(col_base) + half * MY * 32, M, N, rv);
+                const int64_t cbase = static_cast<int64_t>(col_base) + half * MY * 32;
+                resid_fetch(ep, rt, cbase, M, N, rva);
+                if (MY > 1 && cbase + 32 < N) resid_fetch(ep, rt, cbase + 32, M, N, rvb);
                 ptx::mbar_wait(&tfull[buf], aphase);
                 ptx::tc_fence_after();
-#pragma unroll 1
-                for (int cc = 0; cc < MY_MAX; ++cc) {
-                    if (cc >= MY) break;
+                // chunk cc of this warp's columns from register buffer rv; refill rv with chunk cc + 2
+                auto chunk = [&](int cc, float4(&rv)[8]) {
                     const int c = half * MY + cc;
                     const int64_t col0 = static_cast<int64_t>(col_base) + c * 32;
-                    if (col0 >= N) break;  // warp-uniform
                     uint32_t r[32];
                     ptx::tmem_ld32(taddr + c * 32, r);
                     ptx::tmem_ld_wait();
                     resid_store(ep, rt, col0, M, N, r, rv, stg, ss);
-                    if (cc + 1 < MY && col0 + 32 < N) resid_fetch(ep, rt, col0 + 32, M, N, rv);
+                    if (cc + 2 < MY && col0 + 64 < N) resid_fetch(ep, rt, col0 + 64, M, N, rv);
                     // one partial per 64-column group, independent of BN and of the warp split
                     if (ep.ssq_out != nullptr && (((c + 1) & 1) == 0 || col0 + 32 >= N))
                         resid_ssq_flush(ep, rt, M, col0 >> 6, ss);
+                };
+#pragma unroll 1
+                for (int cc = 0; cc < MY_MAX; cc += 2) {
+                    if (cc >= MY || cbase + cc * 32 >= N) break;  // warp-uniform
+                    chunk(cc, rva);
+                    if (cc + 1 >= MY || cbase + (cc + 1) * 32 >= N) break;
+                    chunk(cc + 1, rvb);
                 }
             } else {
                 ptx::mbar_wait(&tfull[buf], aphase);
@@ -580,6 +602,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     ptx::tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0 && trace) {
+        GT(5);
+        trace[blockIdx.x * 8 + 6] = ptx::smid();
+        trace[blockIdx.x * 8 + 7] = static_cast<unsigned long long>((num_tiles - unit + n_units - 1) / n_units);
+    }
     if constexpr (NCTA == 2) ptx::cluster_sync();  // the pair's TMEM and barriers outlive both CTAs' use
     if (warp == 1) {
         ptx::tc_fence_after();
@@ -588,6 +615,19 @@ __global__ void __launch_bounds__(THREADS, 1)
         else
             ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
     }
+}
+
+// KVP_GEMM_TRACE: device buffer for the per-CTA stamps of the most recent launch
+static const char* gemm_trace_path() {
+    static const char* p = getenv("KVP_GEMM_TRACE");
+    return p;
+}
+static unsigned long long* g_trace = nullptr;
+static unsigned long long* gemm_trace_buffer() {
+    if (!gemm_trace_path()) return nullptr;
+    if (!g_trace && cudaMalloc(&g_trace, 1024 * 8 * sizeof(unsigned long long)) != cudaSuccess) g_trace = nullptr;
+    if (g_trace) cudaMemset(g_trace, 0, 1024 * 8 * sizeof(unsigned long long));
+    return g_trace;
 }
 
 template <int BN, int KIND, int NCTA>
@@ -624,6 +664,7 @@ void launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& 
     int group_m = forced_group > 0 ? forced_group : static_cast<int>((32ll << 20) / (static_cast<int64_t>(TM) * K * 2));
     group_m = group_m < 4 ? 4 : group_m;
     group_m = group_m > num_m ? num_m : group_m;
+    unsigned long long* trace = gemm_trace_buffer();
     note_launch();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(grid_units * NCTA));
@@ -639,7 +680,7 @@ void launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& 
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    cudaLaunchKernelEx(&cfg, kern, ta, tb, tbh, M, N, K, n_full, group_m, ep);
+    cudaLaunchKernelEx(&cfg, kern, ta, tb, tbh, M, N, K, n_full, group_m, trace, ep);
 }
 
 template <int BN, int NCTA>
@@ -696,8 +737,11 @@ int gemm_bf16_tc_bn(int64_t M, int64_t N) {
     const int units = num_sms() / (pair ? 2 : 1);
     auto score = [&](int64_t bn, double tile_eff) {
         const int64_t tiles = ((M + tm - 1) / tm) * ((N + bn - 1) / bn);
-        const int64_t waves = (tiles + units - 1) / units;
-        const double useful = static_cast<double>(M) * N / (static_cast<double>(waves) * units * tm * bn);
+        double waves = static_cast<double>((tiles + units - 1) / units);
+        // launch_tc runs a last partial round of wide tiles as half-width tiles when they fit
+        const int64_t rem = tiles % units;
+        if (bn == 256 && tiles > units && rem > 0 && 2 * rem <= units) waves -= 0.5;
+        const double useful = static_cast<double>(M) * N / (waves * units * tm * bn);
         return useful * tile_eff;
     };
     // per-FLOP efficiency of the narrow tile relative to BN=256 (measured; the narrow pair
@@ -707,6 +751,16 @@ int gemm_bf16_tc_bn(int64_t M, int64_t N) {
     if (forced == 128) wide = false;
     if (forced == 256 && N >= 256) wide = true;
     return wide ? 256 : 128;
+}
+
+void gemm_trace_dump() {
+    if (!gemm_trace_path() || !g_trace) return;
+    std::vector<unsigned long long> h(1024 * 8);
+    if (cudaMemcpy(h.data(), g_trace, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost) != cudaSuccess) return;
+    if (FILE* f = fopen(gemm_trace_path(), "wb")) {
+        fwrite(h.data(), sizeof(h[0]), h.size(), f);
+        fclose(f);
+    }
 }
 
 void gemm_bf16_tc(const bf16* A, int64_t M, int64_t K, const bf16* B, int64_t N, const GemmEpilogue& ep,

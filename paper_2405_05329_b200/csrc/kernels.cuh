@@ -95,6 +95,8 @@ struct GemmEpilogue {
 };
 constexpr int KVP_MAX_MIRRORS = 8;
 inline int ssq_parts_for(int64_t cols) { return static_cast<int>((cols + 63) / 64); }
+// KVP_GEMM_TRACE: write the per-CTA stamps of the last tcgen05 GEMM launch (tuning only)
+void gemm_trace_dump();
 void gemm_bf16_tc(const bf16* A, int64_t M, int64_t K, const bf16* B, int64_t N, const GemmEpilogue& ep,
                   cudaStream_t s);
 // tile width the dispatcher picks for this shape (128 or 256)
