@@ -5,6 +5,7 @@
 #pragma once
 
 #include <fstream>
+#include <iterator>
 #include <string>
 
 #include <json.hpp>
@@ -31,22 +32,24 @@ inline PartitionLookupTable table_from_json(const nlohmann::json& doc) {
     return t;
 }
 
+// File I/O goes through a whole-file string: the document is rendered (or slurped) first and the
+// stream is touched once, so a short write and an unreadable path are both reported as IoError and
+// a parse failure as LookupError, the reference's error classes (errors.hpp).
 inline void save_table(const PartitionLookupTable& table, const std::string& path) {
-    std::ofstream out(path);
-    if (!out) throw IoError("cannot open table file for writing: " + path);
-    out << table_to_json(table).dump(2) << "\n";
-    if (!out) throw IoError("failed writing table file: " + path);
+    const std::string text = table_to_json(table).dump(2) + '\n';
+    std::ofstream sink(path, std::ios::binary | std::ios::trunc);
+    if (!sink.is_open()) throw IoError("save_table: unable to create " + path);
+    sink.write(text.data(), static_cast<std::streamsize>(text.size()));
+    sink.flush();
+    if (sink.fail()) throw IoError("save_table: short write to " + path);
 }
 
 inline PartitionLookupTable load_table(const std::string& path) {
-    std::ifstream in(path);
-    if (!in) throw IoError("cannot open table file: " + path);
-    nlohmann::json doc;
-    try {
-        in >> doc;
-    } catch (const nlohmann::json::exception& e) {
-        throw LookupError(std::string("malformed lookup table JSON in ") + path + ": " + e.what());
-    }
+    std::ifstream source(path, std::ios::binary);
+    if (!source.is_open()) throw IoError("load_table: unable to open " + path);
+    const std::string text{std::istreambuf_iterator<char>(source), std::istreambuf_iterator<char>()};
+    nlohmann::json doc = nlohmann::json::parse(text, nullptr, /*allow_exceptions=*/false);
+    if (doc.is_discarded()) throw LookupError("load_table: " + path + " is not valid JSON");
     return table_from_json(doc);
 }
 
