@@ -342,12 +342,17 @@ __device__ __forceinline__ void resid_ssq_flush(const EpiArgs& ep, const ResidT&
     for (int i = 0; i < 8; ++i) ss[i] = 0.f;
 }
 
-// tuning only (KVP_GEMM_TRACE=<file>): per-CTA globaltimer stamps -- 0 entry, 1 prologue done,
-// 2 previous grid complete (PDL), 3 first stage landed, 4 last MMA issued, 5 epilogue done;
-// 6 = SM id, 7 = tiles (scripts/gemm_trace.py)
+// tuning only (build with KVP_NVCC_FLAGS=-DKVP_GEMM_TRACE_ON=1, run with KVP_GEMM_TRACE=<file>):
+// per-CTA globaltimer stamps -- 0 entry, 1 prologue done, 2 previous grid complete (PDL), 3 first
+// stage landed, 4 last MMA issued, 5 epilogue done; 6 = SM id, 7 = tiles (scripts/gemm_trace.py).
+// Compiled out by default: the runtime check inside the converged MMA issue loop cost the
+// QKV / FFN1 GEMMs 4-5 % in isolation and 12 % inside the layer step (profiles/r02/gemm_trace_cost.txt).
+#ifndef KVP_GEMM_TRACE_ON
+#define KVP_GEMM_TRACE_ON 0
+#endif
 #define GT(ev)                                                                  \
     do {                                                                        \
-        if (trace) trace[blockIdx.x * 8 + (ev)] = ptx::globaltimer();           \
+        if (KVP_GEMM_TRACE_ON && trace) trace[blockIdx.x * 8 + (ev)] = ptx::globaltimer(); \
     } while (0)
 
 template <int BN, int KIND, int NCTA>
@@ -491,7 +496,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (int kb = 0; kb < num_kb; ++kb) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
-                    if (t == 0 && kb == 0 && lane == 0) GT(3);
+                    if (KVP_GEMM_TRACE_ON && t == 0 && kb == 0 && lane == 0) GT(3);
                     const uint64_t ad0 = adesc0 + static_cast<uint64_t>((stage * C::A_BYTES) >> 4);
                     const uint64_t bd0 = bdesc0 + static_cast<uint64_t>((stage * C::B_BYTES) >> 4);
 #pragma unroll
@@ -517,7 +522,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 else
                     ptx::mma_commit_w(&tfull[buf]);
             }
-            if (lane == 0) GT(4);
+            if (KVP_GEMM_TRACE_ON && lane == 0) GT(4);
         }
     } else {
         // Epilogue warps 2..9: warp w may touch TMEM lanes [32*(w%4), 32*(w%4)+32); the two
@@ -602,7 +607,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     ptx::tc_fence_before();
     __syncthreads();
-    if (threadIdx.x == 0 && trace) {
+    if (KVP_GEMM_TRACE_ON && threadIdx.x == 0 && trace) {
         GT(5);
         trace[blockIdx.x * 8 + 6] = ptx::smid();
         trace[blockIdx.x * 8 + 7] = static_cast<unsigned long long>((num_tiles - unit + n_units - 1) / n_units);

@@ -1,7 +1,9 @@
 """Per-CTA timeline of the tcgen05 GEMM (KVP_GEMM_TRACE): for one isolated launch of each shape,
 the median over CTAs of entry -> prologue done -> PDL wait -> first stage landed -> last MMA
 issued -> epilogue done, against the ideal MMA time of the CTA's tiles.
-usage: python scripts/gemm_trace.py [shape ...]   (shapes as in scripts/gemm_sweep.py)"""
+usage: python scripts/gemm_trace.py [shape ...]   (shapes as in scripts/gemm_sweep.py)
+The stamps are compiled out of the default build: rebuild with
+KVP_NVCC_FLAGS=-DKVP_GEMM_TRACE_ON=1 first (profiles/r02/gemm_trace_cost.txt)."""
 import json
 import os
 import sys
