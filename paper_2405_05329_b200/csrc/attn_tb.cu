@@ -71,9 +71,12 @@ struct PairArgs {
 };
 
 // trace[ev * 512 + j] = clock() of event ev for key tile j in CTA a.trace_blk
+#ifndef KVP_ATTN_TRACE_ON
+#define KVP_ATTN_TRACE_ON 0  // tuning builds: KVP_NVCC_FLAGS=-DKVP_ATTN_TRACE_ON=1
+#endif
 #define TB_TRACE(ev, j)                                                                                     \
     do {                                                                                                    \
-        if (a.trace && static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x) == a.trace_blk && (j) < 512)   \
+        if (KVP_ATTN_TRACE_ON && a.trace && static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x) == a.trace_blk && (j) < 512)   \
             a.trace[(ev) * 512 + (j)] = static_cast<uint32_t>(clock());                                     \
     } while (0)
 
@@ -112,7 +115,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     float* xm = reinterpret_cast<float*>(smem + Q_BYTES + (KST + VST) * KV_BYTES + BAR_BYTES);  // [BQ] running max
     float* xl = xm + BQ;                                                                      // [2][BQ] row sum by tile parity
 
-    const unsigned long long t_start = a.cta_trace && threadIdx.x == 0 ? gtimer() : 0;
+    const unsigned long long t_start = KVP_ATTN_TRACE_ON && a.cta_trace && threadIdx.x == 0 ? gtimer() : 0;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int h = static_cast<int>(blockIdx.x);
     const int g = h / a.group;
@@ -407,7 +410,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         ptx::tc_fence_after();
         ptx::tmem_dealloc<512>(tmem);
     }
-    if (a.cta_trace && threadIdx.x == 0) {
+    if (KVP_ATTN_TRACE_ON && a.cta_trace && threadIdx.x == 0) {
         unsigned long long* r = a.cta_trace + 4 * (blockIdx.y * gridDim.x + blockIdx.x);
         uint32_t smid;
         asm volatile("mov.u32 %0, %smid;" : "=r"(smid));

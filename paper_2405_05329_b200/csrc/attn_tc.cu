@@ -85,9 +85,12 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 // trace[ev * 512 + j] = clock() of event ev for key tile j, CTA (blockIdx.y * gridDim.x + blockIdx.x) == trace_blk
+#ifndef KVP_ATTN_TRACE_ON
+#define KVP_ATTN_TRACE_ON 0  // tuning builds: KVP_NVCC_FLAGS=-DKVP_ATTN_TRACE_ON=1
+#endif
 #define ATTN_TRACE(ev, j)                                                                              \
     do {                                                                                               \
-        if (a.trace && static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x) == a.trace_blk && (j) < 512) \
+        if (KVP_ATTN_TRACE_ON && a.trace && static_cast<int>(blockIdx.y * gridDim.x + blockIdx.x) == a.trace_blk && (j) < 512) \
             a.trace[(ev) * 512 + (j)] = static_cast<uint32_t>(clock());                                \
     } while (0)
 
@@ -117,7 +120,7 @@ __global__ void __launch_bounds__(threads_for<NT>(), 1)
     uint64_t* o_done = p_full + NT;          // [NT] query tiles
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + NT);
 
-    const unsigned long long t_start = a.cta_trace && threadIdx.x == 0 ? globaltimer() : 0;
+    const unsigned long long t_start = KVP_ATTN_TRACE_ON && a.cta_trace && threadIdx.x == 0 ? globaltimer() : 0;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int num_groups = static_cast<int>((a.q_rows + NT * BQ - 1) / (NT * BQ));
     // grid = (heads, query groups): the block scheduler walks x fastest, so ALL heads of the
@@ -390,7 +393,7 @@ __global__ void __launch_bounds__(threads_for<NT>(), 1)
         ptx::tc_fence_after();
         ptx::tmem_dealloc<TMEM_COLS>(tmem);
     }
-    if (a.cta_trace && threadIdx.x == 0) {
+    if (KVP_ATTN_TRACE_ON && a.cta_trace && threadIdx.x == 0) {
         unsigned long long* r = a.cta_trace + 4 * (blockIdx.y * gridDim.x + blockIdx.x);
         uint32_t smid;
         asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
