@@ -32,6 +32,7 @@ namespace kvp {
 
 bool make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
                     uint32_t box_inner, uint32_t box_outer);
+int num_sms();
 
 namespace {
 using namespace smx;
@@ -516,21 +517,36 @@ void attn_bf16_tc(const bf16* Q, const bf16* K, const bf16* V, bf16* O, const At
         return e ? atoi(e) : 2;
     }();
     const bool h128 = sh.head_dim == 128;
-    // hd 128: the double-buffered one-tile-per-CTA kernel (attn_tb.cu) on grids of up to two
-    // waves of 256-row CTAs -- the rank chunks of KV-Runahead (Llama 4k p=8 last rank: ~650 vs
-    // ~390 TF/s), this kernel's two-tile CTAs on bigger grids (4k p=1 in the full step: 5.8 vs
-    // 5.9 ms; 16k p=1: ~1140 vs ~1040 TF/s).  The two are bitwise identical, so the choice never
-    // changes a row.  KVP_ATTN_TB=0 / 1 forces either.
+    // The double-buffered one-tile-per-CTA kernel (attn_tb.cu) or this kernel's two-tile CTAs:
+    // bitwise identical, so the choice never changes a row.  KVP_ATTN_TB=0 / 1 forces either.
     static const int tb = [] {
         const char* e = getenv("KVP_ATTN_TB");
         return e ? atoi(e) : -1;
     }();
     const int64_t ctas256 = static_cast<int64_t>(sh.n_heads) * ((sh.q_rows + 255) / 256);
     // hd 64 (Falcon) the same way, while this kernel runs its default two 128-key tiles -- the
-    // layout attn_tb restates bit for bit (isolated: Falcon p = 4 / 8 rank chunks 621 / 607 vs
-    // 596 / 578 TF/s; the full 8k grid is a tie in the power-capped step)
+    // layout attn_tb restates bit for bit
     const bool tb_ok = h128 || hd64_tiles == 2;
-    if (tb_ok && (tb == 1 || (tb < 0 && ctas256 <= 2 * 148))) return attn_bf16_tb(Q, K, V, O, sh, s);
+    bool pick_tb;
+    if (sh.offset >= sh.q_rows) {
+        // a later rank's chunk: every CTA walks about the same number of key tiles, so the
+        // choice is wave quantisation -- attn_tb's CTAs are half as tall (twice as many); take it
+        // when its last wave is fuller, or (hd 128) when this kernel's grid is a single partial
+        // wave.  Measured isolated (profiles/r02/attn_select_rank.txt, TF/s tc / tb): Llama rank
+        // chunks of 512 / 1024 / 1280 / 1536 / 1792 / 2048 rows 437/715, 773/815, 674/782,
+        // 801/955, 917/896, 1099/1027; Falcon 512 / 640 / 1024 rows 582/564, 401/497, 623/597 --
+        // the rule picks the faster kernel in all nine.
+        const int64_t sms = num_sms();
+        auto fill = [&](int64_t c) { return static_cast<double>(c) / (((c + sms - 1) / sms) * sms); };
+        const int64_t ctas128 = static_cast<int64_t>(sh.n_heads) * ((sh.q_rows + 127) / 128);
+        const double f_tc = fill(ctas256), f_tb = fill(ctas128);
+        pick_tb = f_tb > 1.02 * f_tc || (h128 && ctas256 <= sms && f_tb >= f_tc);
+    } else {
+        // the causal grid of a first chunk / the serial prompt: longest-first two-tile CTAs on
+        // big grids (4k p = 1 in the full step: 5.8 vs 5.9 ms; 16k: ~1215 vs ~1085 TF/s)
+        pick_tb = ctas256 <= 2 * 148;
+    }
+    if (tb_ok && (tb == 1 || (tb < 0 && pick_tb))) return attn_bf16_tb(Q, K, V, O, sh, s);
     const int np = poly >= 0 ? poly : (h128 ? DEFAULT_POLY_128 : DEFAULT_POLY_64);
     if (h128)
         launch_poly<128, 2, 128>(np, Q, K, V, O, sh, s);

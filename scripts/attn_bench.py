@@ -12,6 +12,10 @@ SHAPES = {  # name: (q_rows, offset, heads, kv_heads, head_dim)
     "llama_4k": (4096, 0, 32, 32, 128), "llama_16k": (16384, 0, 32, 32, 128),
     "llama_4k_p8_last": (512, 3584, 32, 32, 128), "llama_16k_p8_last": (2048, 14336, 32, 32, 128), "falcon_8k": (8192, 0, 71, 1, 64),
     "falcon_8k_p8_last": (1024, 7168, 71, 1, 64), "falcon_8k_p4_last": (2048, 6144, 71, 1, 64),
+    # rank chunks between one and two waves of 256-row CTAs (the attn_tb / attn_tc crossover)
+    "llama_4k_p4_last": (1024, 3072, 32, 32, 128), "llama_rank_1280": (1280, 4096, 32, 32, 128),
+    "llama_rank_1536": (1536, 6144, 32, 32, 128), "llama_rank_1792": (1792, 7168, 32, 32, 128),
+    "falcon_rank_512": (512, 7680, 71, 1, 64), "falcon_rank_640": (640, 7552, 71, 1, 64),
 }
 W = kv.init_weights(kv.ModelConfig(256, 2, 2, 1, 1, "bf16", False))
 tag = ",".join(f"{k[9:]}={v}" for k, v in sorted(os.environ.items()) if k.startswith("KVP_ATTN_"))
