@@ -73,3 +73,26 @@ def test_attention_variant(default, env, bitwise):
         assert res["split_equal"], (env, d)              # split invariance holds in every variant
         if bitwise or (env.get("KVP_ATTN_HD64_TILES") and d == "1024") or (env.get("KVP_ATTN_TB") and "KVP_ATTN_POLY" not in env):
             assert res["hash"] == default[d]["hash"], (env, d)
+
+
+def test_rank_chunk_kernel_selection_split_invariant():
+    """Later-rank chunks pick attn_tc or attn_tb by the wave fill of their grid (attn_tc.cu
+    attn_bf16_tc); whichever they pick, a chunk's rows equal the same rows of the serial (causal,
+    offset 0) launch bit for bit.  Llama-7B attention width (32 heads, hd 128) at 8960 keys:
+    1792 rows at offset 7168 take attn_tc (224 two-tile CTAs), 1280 rows at offset 7680 attn_tb
+    (320 one-tile CTAs against 160 two-tile ones), 512 rows at offset 8448 attn_tb (one partial
+    wave of two-tile CTAs)."""
+    from paper_2405_05329_b200 import kvprefill as kv
+    import oracle as O
+    if kv.device_count() == 0:
+        pytest.skip("no CUDA device")
+    W = kv.init_weights(kv.ModelConfig(4096, 32, 32, 1, 1, "bf16"))
+    C_ = 8960
+    Q = O.random_context(C_, 4096, 41, np.float32) * 4.0
+    K = O.random_context(C_, 4096, 42, np.float32) * 4.0
+    V = O.random_context(C_, 4096, 43, np.float32)
+    full = kv.causal_attention(Q, K, V, kv.CausalMask(0, C_), W)
+    for off in (7168, 7680, 8448):
+        part = kv.causal_attention(Q[off:], K, V, kv.CausalMask(off, C_ - off), W)
+        assert np.array_equal(part, full[off:]), off
+    W.close()
