@@ -263,7 +263,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                 ptx::mbar_wait(&l_ready[(1 - set) * 4 + quarter], ((pend_j - 1) >> 1) & 1);
                 l_prev = xl[((pend_j - 1) & 1) * BQ + xrow];
             }
-            xl[(pend_j & 1) * BQ + xrow] = l_prev * pend_alpha + pend_lsum;
+            // attn_tc.cu's two roundings (l *= alpha, then l += lsum) -- an FFMA here would round
+            // once and break the bitwise equality whenever a row max was re-based at a tile j > 0
+            xl[(pend_j & 1) * BQ + xrow] = __fadd_rn(__fmul_rn(l_prev, pend_alpha), pend_lsum);
             __threadfence_block();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&l_ready[set * 4 + quarter]);

@@ -354,11 +354,11 @@ __global__ void __launch_bounds__(threads_for<NT>(), 1)
                     }
                     ptx::tmem_st_wait();
                 }
-                l *= alpha;
+                l = __fmul_rn(l, alpha);  // explicit roundings: attn_tb.cu restates them
                 m_run = m_new;
             }
             const float lsum = exp_store(sv, m_run, diag);
-            l += lsum;
+            l = __fadd_rn(l, lsum);
             ptx::tmem_st_wait();
             ptx::tc_fence_before();
             __syncwarp();
