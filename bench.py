@@ -460,8 +460,10 @@ def run_multi(args, w, rank, world, local):
                 "config": {"workload": args.workload, **w, "strategy": args.strategy, "partition": list(b),
                            "partition_kind": args.partition, "ranks": world,
                            "transport": ("peer memory: QKV-epilogue stores into the receivers' caches over "
-                                         "NVLink (CUDA IPC) + stream-ordered flags" if args.transport == "peer"
-                                         else "nccl p2p (kvr) / all-gather (tsp)"),
+                                         "NVLink (CUDA IPC) + stream-ordered flags" if tr.peer
+                                         else "nccl p2p (kvr) / all-gather (tsp)"
+                                         + (" (peer transport requested, no CUDA peer access between the "
+                                            "ranks' devices)" if tr.peer_requested else "")),
                            "l2": "flushed (256 MB write) before every step",
                            "parallelism": f"{args.strategy}-p{world}"},
                 "ttft_roofline_frac": (F / (world * peaks["bf16"] * 1e12)) / (ms * 1e-3),

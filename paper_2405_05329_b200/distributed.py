@@ -63,7 +63,25 @@ class Transport:
         self.backend = dist.get_backend(group)
         if peer is None:
             peer = os.environ.get("KVP_TRANSPORT", "") == "peer"
-        self.peer = bool(peer)
+        self.peer = bool(peer) and self._peer_reachable()
+        self.peer_requested = bool(peer)
+
+    def _peer_reachable(self) -> bool:
+        """The peer transport needs every rank's device to reach every other rank's device
+        (same device, or CUDA peer access over NVLink).  Agreed over the group, so all ranks
+        take the same transport (collective: every rank constructs its Transport at the same
+        point); without CUDA the executors are not device-resident and peer_ok() is False."""
+        import torch
+        if not torch.cuda.is_available():
+            return True
+        dist, world = self.dist, self.dist.get_world_size(self.group)
+        dev = torch.cuda.current_device()
+        devs = [None] * world
+        dist.all_gather_object(devs, dev, group=self.group)
+        ok = all(d == dev or torch.cuda.can_device_access_peer(dev, d) for d in devs)
+        votes = [None] * world
+        dist.all_gather_object(votes, ok, group=self.group)
+        return all(votes)
 
     def peer_ok(self, executor) -> bool:
         """The fused peer-memory handoff needs bf16 CUDA executors (tcgen05 QKV epilogue)."""
