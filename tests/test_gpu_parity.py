@@ -90,7 +90,7 @@ def test_reference_accounting_fixtures(fx, prec):  # test_engine.cpp:21-48, acce
 
 # ------------------------------------------------------------ strategy invariance
 @pytest.mark.parametrize("prec", ["f32", "bf16"])
-@pytest.mark.parametrize("d,h,kvh", [(16, 4, 2), (32, 4, 4), (256, 2, 2), (512, 4, 1), (1024, 8, 8)])
+@pytest.mark.parametrize("d,h,kvh", [(16, 4, 2), (32, 4, 4), (256, 2, 2), (512, 4, 1), (512, 8, 2), (1024, 8, 8)])
 def test_strategies_bitwise_identical(prec, d, h, kvh):  # test_engine.cpp:50-99
     W = engine(d, h, kvh, 2, 3, prec, True)
     rng = np.random.default_rng(d + h)
