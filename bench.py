@@ -318,6 +318,88 @@ def kv_handoff_bandwidth_peer(b, w, rank, world, ex, reps=10):
     return out[0]
 
 
+def noise_sidecar_study(args, w, rank, world, local, run_step, runs, sim):
+    """The reference's noise study (NoiseSidecar + noise_study, simnet.hpp:65-78,
+    332-353) with REAL background traffic.  Per trial the reference's seeded draw
+    (NoiseSidecar.for_trial / degraded_link) picks one adjacent link i -> i+1 for every layer
+    slot; during that slot rank i streams background copies into rank i+1's memory (CUDA IPC
+    peer mapping, copy engine, a side stream) at (1 - 1/F) of the 900 GB/s link, so the link
+    is left roughly bandwidth / F for the handoff.  Slots are quiet TTFT / L long from the
+    run's start (host-timed: an approximation of the simulator's per-layer draw).
+    Degradation = (noisy - quiet) / quiet per trial, beside the simulator's noise_study on the
+    calibrated cost model (`sim`)."""
+    import ctypes as C
+    import threading
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_05329_b200 import kvprefill as kv
+    from paper_2405_05329_b200.distributed import _ipc_export
+
+    F, T, L = args.noise_factor, args.noise_trials, w["n_layers"]
+    chunk = 32 << 20
+    src_buf = torch.empty(chunk, dtype=torch.uint8, device=f"cuda:{local}")
+    sink = torch.empty(chunk, dtype=torch.uint8, device=f"cuda:{local}")
+    handles = [None] * world
+    dist.all_gather_object(handles, _ipc_export(sink.data_ptr()))
+    peer_base, peer = None, None
+    if rank + 1 < world:
+        ptr = C.c_void_p()
+        kv._check(kv.lib().kvp_ipc_open(handles[rank + 1][0], 0, C.byref(ptr)), "ipc_open")
+        peer_base = int(ptr.value)
+        peer = peer_base + handles[rank + 1][1]
+    side = torch.cuda.Stream(device=local)
+    out = {"factor": F, "trials": T, "seed": args.noise_seed, "links": world - 1,
+           "what": "background peer copies on the reference's seeded per-layer link draw, (1 - 1/F) of 900 GB/s"}
+    try:
+        for name, (strat, part, quiet_ms) in runs.items():
+            slot_s = quiet_ms * 1e-3 / L
+            per_slot = int(slot_s * 900e9 * (1.0 - 1.0 / F))
+            noisy, injected = [], 0
+            for t in range(T):
+                sc = kv.NoiseSidecar.for_trial(args.noise_seed, t, F)
+                mine = [layer for layer in range(L) if sc.degraded_link(layer, world - 1) == rank]
+
+                def traffic(t0, mine=mine):
+                    nonlocal injected
+                    for layer in mine:
+                        delay = t0 + layer * slot_s - time.perf_counter()
+                        if delay > 0:
+                            time.sleep(delay)
+                        n = per_slot
+                        while n > 0:
+                            k = min(n, chunk)
+                            kv._check(kv.lib().kvp_stream_copy(C.c_void_p(side.cuda_stream), C.c_void_p(peer),
+                                                               C.c_void_p(src_buf.data_ptr()), k), "stream_copy")
+                            injected += k
+                            n -= k
+
+                def hook():
+                    th = threading.Thread(target=traffic, args=(time.perf_counter(),))
+                    th.start()
+                    return th
+
+                th, res = run_step(strat, part, hook)
+                th.join()
+                side.synchronize()
+                noisy.append(res.ttft_ms)
+            deg = [(x - quiet_ms) / quiet_ms for x in noisy]
+            out[name] = {"quiet_ms": quiet_ms, "noisy_ms": noisy, "degradation": deg,
+                         "mean_degradation": statistics.mean(deg), "max_degradation": max(deg),
+                         "slot_ms": slot_s * 1e3, "bytes_per_slot": per_slot}
+            tot = torch.tensor([float(injected)], dtype=torch.float64,
+                               device=f"cuda:{local}" if dist.get_backend() == "nccl" else "cpu")
+            dist.all_reduce(tot)
+            out[name]["injected_bytes_total"] = float(tot.item())
+    finally:
+        dist.barrier()
+        if peer_base is not None:
+            kv.lib().kvp_ipc_close(C.c_void_p(peer_base), 0)
+    out["simulated"] = sim
+    return out
+
+
 def run_multi(args, w, rank, world, local):
     """One process per GPU: KVR chain / TSP all-gather over NVLink through the distributed
     driver.  The line carries the north-star comparison on the same kernels: KVR even split,
@@ -351,7 +433,12 @@ def run_multi(args, w, rank, world, local):
         kv_dim = w["n_kv_heads"] * (w["d_model"] // w["n_heads"])
         net = kv.NetworkModel(bandwidth=770e9 / (2 * kv_dim * 2), latency=10e-6)
         found = kv.search_partition(C, world, cfg, cost, net).partition
-        obj = [{"b": list(found.boundaries),
+        sim_noise = None
+        if args.noise_factor > 1:  # the reference's noise_study on the calibrated costs
+            sim_noise = {k: kv.noise_study(st, pt, cfg, cost, net, args.noise_factor, args.noise_trials,
+                                           args.noise_seed).__dict__
+                         for k, st, pt in (("kvr_s", KVR, found), ("tsp", TSP, even))}
+        obj = [{"b": list(found.boundaries), "sim_noise": sim_noise,
                 "sim_ms": {k: 1e3 * kv.simulate_ttft(st, pt, cfg, cost, net)
                            for k, st, pt in (("kvr_even", KVR, even), ("kvr_s", KVR, found), ("tsp", TSP, even))}}]
     dist.broadcast_object_list(obj, src=0)
@@ -376,6 +463,14 @@ def run_multi(args, w, rank, world, local):
         bb = pt.boundaries
         return run_rank(strat, ctx_dev[bb[rank]:bb[rank + 1]] if rows is None else rows, pt, ex, tr, rank, world,
                         w["n_layers"])
+
+    def hooked_step(strat, pt, hook):  # the noise sidecar starts with the run
+        flush.zero_()
+        torch.cuda.synchronize()
+        dist.barrier()
+        bb = pt.boundaries
+        th = hook()
+        return th, run_rank(strat, ctx_dev[bb[rank]:bb[rank + 1]], pt, ex, tr, rank, world, w["n_layers"])
 
     for _ in range(args.warmup):
         step(strategy, part)
@@ -418,6 +513,17 @@ def run_multi(args, w, rank, world, local):
             table[k]["simulated_ms"] = v
         table["kvr_s_over_tsp"] = table["tsp"]["ttft_ms"] / table["kvr_s"]["ttft_ms"]
         table["kvr_s_over_kvr_even"] = table["kvr_even"]["ttft_ms"] / table["kvr_s"]["ttft_ms"]
+    noise = None
+    if args.noise_factor > 1 and world > 1:
+        if not tr.peer or table is None:
+            noise = {"skipped": "needs the strategy table and CUDA peer access between the ranks' devices"}
+        else:
+            try:
+                noise = noise_sidecar_study(args, w, rank, world, local, hooked_step,
+                                            {"kvr_s": (KVR, searched, table["kvr_s"]["ttft_ms"]),
+                                             "tsp": (TSP, even, table["tsp"]["ttft_ms"])}, obj[0]["sim_noise"])
+            except Exception as err:  # the study must never break the TTFT line
+                noise = {"error": str(err)}
     W.set_profiling(True)
     step(strategy, part)
     stats = W.kernel_stats()
@@ -476,6 +582,7 @@ def run_multi(args, w, rank, world, local):
                 "clocks": clocks[0], "clocks_all": clocks,
                 "gpu_launches": sum(all_launches),
                 "kv_handoff": handoff,
+                "noise_sidecar": noise,
                 "e2e": {"value": statistics.mean(e2e_t), "unit": "ms", "h2d_bytes_per_step": C * w["d_model"] * 4,
                         "d2h_bytes_per_step": C * w["d_model"] * 4,
                         "clock": "host perf_counter per rank around run_rank (pinned chunk H2D, prefill, hidden "
@@ -597,6 +704,10 @@ def main():
     ap.add_argument("--strategy", default="kvr", choices=["kvr", "tsp"])
     ap.add_argument("--partition", default="even", choices=["even", "search"])
     ap.add_argument("--transport", default="peer", choices=["peer", "msg"])
+    ap.add_argument("--noise-factor", type=float, default=0.0,
+                    help="N>1: physical noise study (SURVEY 8f #2) with this slowdown factor (> 1)")
+    ap.add_argument("--noise-trials", type=int, default=3)
+    ap.add_argument("--noise-seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-decode", action="store_true")

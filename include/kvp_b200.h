@@ -329,6 +329,11 @@ kvp_status kvp_noise_study(int32_t strategy, int64_t C, const int64_t* boundarie
                            const kvp_cost_model* cost, const kvp_network_model* net, double slowdown_factor,
                            int64_t trials, uint64_t seed, double* quiet_ttft, double* mean_degradation,
                            double* max_degradation, double* per_trial);
+/* NoiseSidecar::degraded_link (simnet.hpp:71-75): the adjacent link (i -> i+1) a sidecar with
+ * this seed slows in `layer`, -1 without links; noise_study's per-trial sidecar seed
+ * mix_seed(seed, 0x7472, trial) (simnet.hpp:343).  Used by the physical sidecar of bench.py. */
+kvp_status kvp_noise_degraded_link(uint64_t sidecar_seed, int64_t layer, int64_t link_count, int64_t* link_out);
+kvp_status kvp_noise_trial_seed(uint64_t study_seed, int64_t trial, uint64_t* sidecar_seed_out);
 /* KVR-P: PartitionLookupTable (lookup_table.hpp:22-39) given as n entries of
  * (context_lengths[i], ratios[i*p .. i*p+p)); interpolate_partition (lookup_table.hpp:44-64)
  * and partition_from_table (lookup_table.hpp:68-70). */

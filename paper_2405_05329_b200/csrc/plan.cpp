@@ -567,6 +567,25 @@ kvp_status kvp_noise_study(int32_t strategy, int64_t C, const int64_t* b, int64_
     });
 }
 
+kvp_status kvp_noise_degraded_link(uint64_t sidecar_seed, int64_t layer, int64_t link_count, int64_t* link_out) {
+    return guard([&] {
+        if (!link_out) throw Error(KVP_ERR_INPUT, "null argument");
+        if (link_count < 1) {
+            *link_out = -1;
+            return;
+        }
+        uint64_t st = mix(sidecar_seed, 0x6e6fu, static_cast<uint64_t>(layer));
+        *link_out = static_cast<int64_t>(sm_next(st) % static_cast<uint64_t>(link_count));
+    });
+}
+
+kvp_status kvp_noise_trial_seed(uint64_t study_seed, int64_t trial, uint64_t* sidecar_seed_out) {
+    return guard([&] {
+        if (!sidecar_seed_out) throw Error(KVP_ERR_INPUT, "null argument");
+        *sidecar_seed_out = mix(study_seed, 0x7472u, static_cast<uint64_t>(trial));
+    });
+}
+
 // PartitionLookupTable::insert validation (lookup_table.hpp:26-38) + interpolate_partition.
 static std::vector<double> interpolate(const int64_t* Cs, const double* ratios, int64_t n, int64_t p, int64_t C) {
     if (p < 1) throw Error(KVP_ERR_LOOKUP, "table process count not set");

@@ -169,6 +169,8 @@ _SIGS = {
                                               C.POINTER(_SearchCfg), _I64P, C.POINTER(_SearchRes)]),
     "kvp_simulate_ttft_noisy": (C.c_int, [C.c_int32, C.c_int64, _I64P, C.c_int64, C.c_int64, C.POINTER(_Cost),
                                           C.POINTER(_Net), C.c_uint64, C.c_double, C.POINTER(C.c_double)]),
+    "kvp_noise_degraded_link": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, C.POINTER(C.c_int64)]),
+    "kvp_noise_trial_seed": (C.c_int, [C.c_uint64, C.c_int64, C.POINTER(C.c_uint64)]),
     "kvp_noise_study": (C.c_int, [C.c_int32, C.c_int64, _I64P, C.c_int64, C.c_int64, C.POINTER(_Cost),
                                   C.POINTER(_Net), C.c_double, C.c_int64, C.c_uint64, C.POINTER(C.c_double),
                                   C.POINTER(C.c_double), C.POINTER(C.c_double), _P]),
@@ -884,6 +886,20 @@ class NoiseSidecar:
     bandwidth / slowdown_factor."""
     seed: int = 1
     slowdown_factor: float = 1.0
+
+    def degraded_link(self, layer: int, link_count: int) -> int:
+        """simnet.hpp:71-75: the adjacent link (i -> i+1) slowed in `layer` (-1 without links)."""
+        out = C.c_int64()
+        _check(lib().kvp_noise_degraded_link(C.c_uint64(self.seed), layer, link_count, C.byref(out)),
+               "noise_degraded_link")
+        return int(out.value)
+
+    @staticmethod
+    def for_trial(study_seed: int, trial: int, slowdown_factor: float) -> "NoiseSidecar":
+        """noise_study's sidecar of trial t: seed mix_seed(seed, 0x7472, t) (simnet.hpp:342-344)."""
+        out = C.c_uint64()
+        _check(lib().kvp_noise_trial_seed(C.c_uint64(study_seed), trial, C.byref(out)), "noise_trial_seed")
+        return NoiseSidecar(int(out.value), slowdown_factor)
 
 
 def simulate_ttft_noisy(strategy: Strategy, partition: ContextPartition, model: ModelConfig, cost: CostModel,

@@ -134,6 +134,28 @@ def test_bench_multi_rank_path_on_one_gpu():
             assert d["e2e"]["value"] > 0
 
 
+def test_bench_noise_sidecar_on_one_gpu():
+    """bench.py's physical noise study: the reference's seeded per-layer link
+    draw drives real background copies into the next rank's memory during the KVR-S and TSP
+    runs; the line carries per-trial degradations beside the simulator's noise_study."""
+    import json
+    import subprocess
+    env = dict(os.environ, KVP_BENCH_SHARE_GPU="1", KVP_BENCH_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "3",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+                        os.path.join(ROOT, "bench.py"), "--gpus", "3", "--workload", "tiny", "--steps", "2",
+                        "--warmup", "3", "--no-e2e", "--noise-factor", "2", "--noise-trials", "2"],
+                       capture_output=True, text=True, env=env, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
+    ns = d["noise_sidecar"]
+    assert "error" not in ns and "skipped" not in ns, ns
+    for k in ("kvr_s", "tsp"):
+        assert len(ns[k]["noisy_ms"]) == 2 and all(x > 0 for x in ns[k]["noisy_ms"])
+        assert ns[k]["injected_bytes_total"] > 0
+        assert len(ns["simulated"][k]["per_trial"]) == 2
+
+
 def test_bench_single_process_ranks_table():
     """python bench.py --gpus 1 --ranks 4: the in-process engine with 4 ranks on one GPU; the
     line carries KVR even / KVR-S / TSP TTFTs on the same kernels and the busiest link's

@@ -283,3 +283,32 @@ def test_causal_cost_model_extension():
     assert sum(sizes) == 8192
     assert all(sizes[i] >= sizes[i + 1] for i in range(3))
     assert found.ttft <= kv.simulate_ttft_causal(kv.Strategy.KVR, even, m, cost, net)
+
+
+def test_noise_sidecar_link_draw():  # simnet.hpp:65-78, 342-344; rng.hpp:10-37
+    """The physical sidecar (bench.py --noise-factor) slows exactly the links the reference's
+    NoiseSidecar draws: restated here from rng.hpp's SplitMix64 / mix_seed."""
+    M = (1 << 64) - 1
+
+    def nxt(state):
+        state = (state + 0x9E3779B97F4A7C15) & M
+        z = state
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+        return state, z ^ (z >> 31)
+
+    def mix_seed(base, a, b=0):
+        _, s = nxt(base)
+        s ^= (a * 0xD1342543DE82EF95) & M
+        _, h = nxt(s)
+        return h ^ ((b * 0xAF251AF3B0F025B5) & M)
+
+    for study_seed in (1, 7, 2**63 + 5):
+        for t in range(4):
+            sc = kv.NoiseSidecar.for_trial(study_seed, t, 2.0)
+            assert sc.seed == mix_seed(study_seed, 0x7472, t) and sc.slowdown_factor == 2.0
+            for links in (1, 3, 7):
+                for layer in range(6):
+                    _, r = nxt(mix_seed(sc.seed, 0x6E6F, layer))
+                    assert sc.degraded_link(layer, links) == r % links
+    assert kv.NoiseSidecar(3, 2.0).degraded_link(0, 0) == -1
