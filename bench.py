@@ -343,12 +343,22 @@ def noise_sidecar_study(args, w, rank, world, local, run_step, runs, sim):
     sink = torch.empty(chunk, dtype=torch.uint8, device=f"cuda:{local}")
     handles = [None] * world
     dist.all_gather_object(handles, _ipc_export(sink.data_ptr()))
-    peer_base, peer = None, None
-    if rank + 1 < world:
-        ptr = C.c_void_p()
-        kv._check(kv.lib().kvp_ipc_open(handles[rank + 1][0], 0, C.byref(ptr)), "ipc_open")
-        peer_base = int(ptr.value)
-        peer = peer_base + handles[rank + 1][1]
+    peer_base, peer, setup_err = None, None, None
+    try:
+        if rank + 1 < world:
+            ptr = C.c_void_p()
+            kv._check(kv.lib().kvp_ipc_open(handles[rank + 1][0], 0, C.byref(ptr)), "ipc_open")
+            peer_base = int(ptr.value)
+            peer = peer_base + handles[rank + 1][1]
+    except Exception as err:
+        setup_err = str(err)
+    # every rank runs the trials or none does (the runs are collective)
+    errs = [None] * world
+    dist.all_gather_object(errs, setup_err)
+    if any(errs):
+        if peer_base is not None:
+            kv.lib().kvp_ipc_close(C.c_void_p(peer_base), 0)
+        return {"skipped": "sidecar mapping failed: " + "; ".join(e for e in errs if e)}
     side = torch.cuda.Stream(device=local)
     out = {"factor": F, "trials": T, "seed": args.noise_seed, "links": world - 1,
            "what": "background peer copies on the reference's seeded per-layer link draw, (1 - 1/F) of 900 GB/s"}
