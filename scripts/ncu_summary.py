@@ -25,7 +25,7 @@ KEYS = {
     "grid": "launch__grid_size",
     "block": "launch__block_size",
 }
-SCALE = {"Mbyte": 1e6, "Kbyte": 1e3, "Gbyte": 1e9, "byte": 1.0, "usecond": 1.0, "msecond": 1e3, "nsecond": 1e-3,
+SCALE = {"ms": 1e3, "us": 1.0, "ns": 1e-3, "Mbyte": 1e6, "Kbyte": 1e3, "Gbyte": 1e9, "byte": 1.0, "usecond": 1.0, "msecond": 1e3, "nsecond": 1e-3,
          "Ghz": 1.0, "cycle/nsecond": 1.0, "cycle/usecond": 1e-3}
 
 
